@@ -1,0 +1,126 @@
+"""Per-head pattern configuration (input data, not arithmetic).
+
+The paper's offline search (Alg.4) emits, per head, a boundary type
+(No/K/Q/2D-Boundary) and one intra-modality pattern per modality or
+one pattern per (query-modality, key-modality) pair.  The parameter tuples are
+those of `tab:search_space`:
+  Grid    (stride, use_hline, use_vline, use_slash, max_stride)
+  A-shape (sink, local)
+  VS      (vertical size, slash size)
+Readings C7/C8/C17: Grid also carries a
+sink and a local window (default 128/128); stride>0 means a fixed frame_stride,
+stride==0 means "search [stride_min, stride_max]".
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+KIND_NONE, KIND_FULL, KIND_ASHAPE, KIND_VSLASH, KIND_GRID = 0, 1, 2, 3, 4
+BND_NONE, BND_K, BND_Q, BND_2D = 0, 1, 2, 3
+MAX_MOD = 4
+
+KIND_NAMES = {KIND_NONE: "none", KIND_FULL: "full", KIND_ASHAPE: "ashape",
+              KIND_VSLASH: "vslash", KIND_GRID: "grid"}
+BND_NAMES = {BND_NONE: "none", BND_K: "k", BND_Q: "q", BND_2D: "2d"}
+
+
+@dataclass(frozen=True)
+class Pattern:
+    kind: int = KIND_NONE
+    sink: int = 0
+    local: int = 0
+    n_vertical: int = 0
+    n_slash: int = 0
+    stride: int = 0          # Grid: >0 fixed (frame_stride); 0 => search
+    stride_min: int = 2
+    stride_max: int = 1024
+    use_hline: bool = False
+    use_vline: bool = False
+    use_slash: bool = False
+
+    def describe(self) -> str:
+        k = KIND_NAMES[self.kind]
+        if self.kind == KIND_ASHAPE:
+            return f"ashape({self.sink},{self.local})"
+        if self.kind == KIND_VSLASH:
+            return f"vs({self.n_vertical},{self.n_slash})"
+        if self.kind == KIND_GRID:
+            st = self.stride if self.stride > 0 else f"[{self.stride_min},{self.stride_max}]"
+            fl = "".join(c for c, f in zip("hvs", (self.use_hline, self.use_vline, self.use_slash)) if f)
+            return f"grid({st},{fl},sink={self.sink},local={self.local})"
+        return k
+
+
+def ashape(sink: int = 128, local: int = 4096) -> Pattern:
+    return Pattern(kind=KIND_ASHAPE, sink=sink, local=local)
+
+
+def vslash(n_vertical: int, n_slash: int) -> Pattern:
+    return Pattern(kind=KIND_VSLASH, n_vertical=n_vertical, n_slash=n_slash)
+
+
+def grid(stride: int = 0, h: bool = True, v: bool = True, sl: bool = False,
+         sink: int = 128, local: int = 128, stride_min: int = 2, stride_max: int = 1024) -> Pattern:
+    return Pattern(kind=KIND_GRID, stride=stride, stride_min=stride_min, stride_max=stride_max,
+                   use_hline=h, use_vline=v, use_slash=sl, sink=sink, local=local)
+
+
+def full() -> Pattern:
+    return Pattern(kind=KIND_FULL)
+
+
+def none() -> Pattern:
+    return Pattern(kind=KIND_NONE)
+
+
+@dataclass
+class HeadConfig:
+    """One head: boundary type + intra patterns (per query modality) or pair patterns."""
+    boundary: int = BND_NONE
+    intra: List[Pattern] = field(default_factory=lambda: [none()] * MAX_MOD)
+    pair: List[List[Pattern]] = field(default_factory=lambda: [[none()] * MAX_MOD for _ in range(MAX_MOD)])
+
+    @staticmethod
+    def no_boundary(p: Pattern) -> "HeadConfig":
+        intra = [none()] * MAX_MOD
+        intra[0] = p
+        return HeadConfig(boundary=BND_NONE, intra=intra)
+
+    @staticmethod
+    def q_boundary(per_mod: List[Pattern]) -> "HeadConfig":
+        intra = list(per_mod) + [none()] * (MAX_MOD - len(per_mod))
+        return HeadConfig(boundary=BND_Q, intra=intra)
+
+    @staticmethod
+    def two_d(pairs: List[List[Pattern]]) -> "HeadConfig":
+        pr = [[none()] * MAX_MOD for _ in range(MAX_MOD)]
+        for a, row in enumerate(pairs):
+            for b, p in enumerate(row):
+                pr[a][b] = p
+        return HeadConfig(boundary=BND_2D, pair=pr)
+
+    def describe(self) -> str:
+        if self.boundary in (BND_NONE, BND_K):
+            return f"{BND_NAMES[self.boundary]}:{self.intra[0].describe()}"
+        if self.boundary == BND_Q:
+            return "q:" + "|".join(p.describe() for p in self.intra if p.kind != KIND_NONE)
+        return "2d:" + ";".join(
+            f"{a}{b}={self.pair[a][b].describe()}" for a in range(MAX_MOD) for b in range(MAX_MOD)
+            if self.pair[a][b].kind != KIND_NONE)
+
+
+@dataclass(frozen=True)
+class Problem:
+    n_heads: int
+    n_kv_heads: int
+    seq_len: int
+    head_dim: int
+    n_modalities: int = 1
+    last_q: int = 64          # P:412 "we set last_q = 64"
+    block: int = 128          # reading C19
+    scale: float = 0.0        # 0 => 1/sqrt(D)
+
+    @property
+    def tau(self) -> float:
+        return self.scale if self.scale > 0 else 1.0 / (self.head_dim ** 0.5)
