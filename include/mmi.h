@@ -1,0 +1,148 @@
+/* mmi.h — C ABI of the B200 (sm_100a) MMInference sparse pre-fill library.
+ *
+ * Operation (PAPER.md, arXiv 2504.16083): modality-aware permutation sparse
+ * attention for pre-fill.  Per attention head, an online sparse index is
+ * estimated from the last query rows (Alg.1), the
+ * tensors are permuted (Alg.1, Alg.2, Alg.3), block-sparse
+ * causal FlashAttention runs over the selected key tiles (Alg.5-7),
+ * and the output is scattered back to token order (Alg.6, Alg.7).
+ *
+ * Conventions (all entry points):
+ *  - Every tensor pointer is a DEVICE pointer owned by the caller, unless the
+ *    parameter name ends in _host.  Layouts are contiguous row-major:
+ *      q [H, S, D] bf16, k/v [Hkv, S, D] bf16, o [H, S, D] bf16,
+ *      lse [H, S] fp32 (natural log of the softmax normaliser), modality [S] u8.
+ *  - GQA: query head h reads KV head h / (H / Hkv)  (reading: Qwen2 convention;
+ *    the paper is silent).
+ *  - All calls are asynchronous on `stream`; none synchronises the device,
+ *    allocates or frees, except mmi_export_index (test only: synchronises).
+ *  - Scratch and the sparse index live in a caller-provided workspace of at
+ *    least mmi_workspace_bytes(problem, cfg_host) bytes (256-byte aligned).  The
+ *    same (problem, cfg_host) must be passed to every call of one pass.
+ *  - Errors: arguments are validated on the host before any launch; a non-OK
+ *    status is returned and mmi_last_error() gives a thread-local message.
+ *    Launch failures return MMI_E_CUDA.  Nothing is launched on error.
+ *  - Deterministic: the same inputs give a bit-identical index and output.
+ */
+#ifndef MMI_H_
+#define MMI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* mmi_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  MMI_OK = 0,
+  MMI_E_INVALID = 1,     /* null pointer, bad enum value                          */
+  MMI_E_SHAPE = 2,       /* H % Hkv != 0, D not in {64,128}, S < 1, ...            */
+  MMI_E_CONFIG = 3,      /* pattern config invalid (see mmi_pattern)               */
+  MMI_E_UNSUPPORTED = 4, /* n_modalities > MMI_MAX_MOD, stride > 1024, ...         */
+  MMI_E_WORKSPACE = 5,   /* workspace null, misaligned or too small                */
+  MMI_E_CUDA = 6         /* a CUDA launch / tensor-map creation failed             */
+} mmi_status;
+
+/* Pattern kinds ("A-shape, Vertical-Slash and Grid" + FULL / NONE). */
+typedef enum { MMI_PAT_NONE = 0, MMI_PAT_FULL = 1, MMI_PAT_ASHAPE = 2, MMI_PAT_VSLASH = 3, MMI_PAT_GRID = 4 } mmi_kind;
+/* Boundary types. K-boundary executes as No-boundary. */
+typedef enum { MMI_BND_NONE = 0, MMI_BND_K = 1, MMI_BND_Q = 2, MMI_BND_2D = 3 } mmi_boundary;
+
+/* One pattern (tab:search_space).
+ *  ASHAPE: admits key y of query x iff y < sink or x - y < local   (local >= 1)
+ *  VSLASH: n_vertical columns + n_slash diagonals chosen online from the
+ *          last-64-query estimate; column 0 and offset 0 forced.
+ *          Cross-modality pairs of 2D heads: verticals only (n_slash = 0).
+ *  GRID:   stride > 0 = fixed frame_stride (phase searched); stride == 0 =
+ *          search stride in [stride_min, stride_max] (max 1024).
+ *          use_hline / use_vline / use_slash select the lines;
+ *          sink / local (>= 1) add the first keys and the causal band (reading C8). */
+typedef struct {
+  int32_t kind;
+  int32_t sink, local;
+  int32_t n_vertical, n_slash;
+  int32_t stride, stride_min, stride_max;
+  uint8_t use_hline, use_vline, use_slash, _pad;
+} mmi_pattern;
+
+#define MMI_MAX_MOD 4
+
+/* Per-head configuration, the output of the offline search (Alg.4).
+ *  NONE/K : intra[0] applies to all rows in original coordinates.
+ *  Q      : intra[m] applies to query rows of modality m, original coordinates
+ *           (Alg.2, reading C12).
+ *  2D     : pair[a][b] applies to query modality a x key modality b; a == b in
+ *           modality-rank coordinates, a != b in original coordinates with kinds
+ *           NONE / FULL / ASHAPE / VSLASH(n_slash = 0) (Alg.3, C13).
+ *           pair[a][a] must not be NONE for a present modality. */
+typedef struct {
+  int32_t boundary;
+  mmi_pattern intra[MMI_MAX_MOD];
+  mmi_pattern pair[MMI_MAX_MOD][MMI_MAX_MOD];
+} mmi_head_config;
+
+typedef struct {
+  int32_t n_heads, n_kv_heads, seq_len, head_dim; /* H, Hkv, S, D (D in {64, 128})        */
+  int32_t n_modalities;                           /* labels must be < n_modalities        */
+  int32_t last_q;                                 /* estimation rows, 64          */
+  int32_t block;                                  /* 128 (reading C19); only 128 supported */
+  float scale;                                    /* 0 => 1/sqrt(D)               */
+} mmi_problem;
+
+/* Bytes of device workspace needed for (problem, cfg_host[0..H-1]).  0 on invalid input. */
+size_t mmi_workspace_bytes(const mmi_problem* problem, const mmi_head_config* cfg_host);
+
+/* Step a1-a5: modality bookkeeping, last_q slab estimation, VS
+ * top-k, grid stride/phase search and index (view + tile list) construction.
+ * Reads q, k, modality; writes only the workspace. */
+mmi_status mmi_estimate_index(const mmi_problem* problem, const mmi_head_config* cfg_host,
+                              const void* q, const void* k, const uint8_t* modality,
+                              void* ws, size_t ws_bytes, mmi_stream_t stream);
+
+/* Step a6: gather the permuted Q̄ / K̄ / V̄ views the index needs into the
+ * workspace (pads zero-filled).  Requires mmi_estimate_index on the same ws. */
+mmi_status mmi_permute(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws, size_t ws_bytes,
+                       const void* q, const void* k, const void* v, mmi_stream_t stream);
+
+/* Step a7: block-sparse causal attention over every work item of the index
+ * (tcgen05 / TMEM / TMA kernel).  Rows owned by a single pass are written to
+ * o / lse directly; rows with several passes leave fp32 partials in ws.
+ * lse may be NULL. */
+mmi_status mmi_sparse_prefill(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws,
+                              size_t ws_bytes, const void* q, const void* k, const void* v, void* o, float* lse,
+                              mmi_stream_t stream);
+
+/* Step a8: LSE-merge the partial rows and scatter them to token order in o / lse.
+ * After this call o [H,S,D] holds the complete sparse attention output. */
+mmi_status mmi_unpermute(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws, size_t ws_bytes,
+                         void* o, float* lse, mmi_stream_t stream);
+
+/* Same-build dense causal attention (the comparator), same kernel and tiles. */
+mmi_status mmi_dense_prefill(const mmi_problem* problem, const void* q, const void* k, const void* v, void* o,
+                             float* lse, mmi_stream_t stream);
+
+/* TEST ONLY (synchronises the stream).  Copies the estimated index of head h
+ * to host_buf as int32 words: see mmi_export_layout in the Python binding.
+ * Returns the number of int32 words needed when host_buf is NULL (via *words). */
+mmi_status mmi_export_index(const mmi_problem* problem, const mmi_head_config* cfg_host, const void* ws,
+                            size_t ws_bytes, int32_t head, int32_t* host_buf, size_t* words, mmi_stream_t stream);
+
+/* TEST ONLY: per-row admitted-key fingerprints (count, sum pos, sum pos^2) of
+ * the sparse pass, int64 [H, S, 3] device buffer (zeroed by the caller). */
+mmi_status mmi_sparse_fingerprint(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws,
+                                  size_t ws_bytes, const void* q, const void* k, const void* v, int64_t* fp,
+                                  mmi_stream_t stream);
+
+/* Thread-local message for the last non-OK status of this thread. */
+const char* mmi_last_error(void);
+
+/* Library version string. */
+const char* mmi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMI_H_ */

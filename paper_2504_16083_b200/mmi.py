@@ -1,0 +1,209 @@
+"""Thin ctypes binding of include/mmi.h (argument marshalling only).
+
+Every step of the hot path runs in libmmi.so (CUDA kernels for sm_100a); this
+module only converts torch tensors / config dataclasses to pointers and C
+structs.  There is no CPU fallback: if the shared library or a CUDA device is
+missing, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence
+
+import torch
+
+from synth.config import HeadConfig, Pattern, Problem, MAX_MOD
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmmi.so")
+
+MMI_OK = 0
+STATUS = {0: "MMI_OK", 1: "MMI_E_INVALID", 2: "MMI_E_SHAPE", 3: "MMI_E_CONFIG", 4: "MMI_E_UNSUPPORTED",
+          5: "MMI_E_WORKSPACE", 6: "MMI_E_CUDA"}
+
+
+class MMIError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class c_pattern(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("sink", ctypes.c_int32), ("local", ctypes.c_int32),
+                ("n_vertical", ctypes.c_int32), ("n_slash", ctypes.c_int32), ("stride", ctypes.c_int32),
+                ("stride_min", ctypes.c_int32), ("stride_max", ctypes.c_int32),
+                ("use_hline", ctypes.c_uint8), ("use_vline", ctypes.c_uint8), ("use_slash", ctypes.c_uint8),
+                ("_pad", ctypes.c_uint8)]
+
+
+class c_head_config(ctypes.Structure):
+    _fields_ = [("boundary", ctypes.c_int32), ("intra", c_pattern * MAX_MOD),
+                ("pair", (c_pattern * MAX_MOD) * MAX_MOD)]
+
+
+class c_problem(ctypes.Structure):
+    _fields_ = [("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32), ("seq_len", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("n_modalities", ctypes.c_int32), ("last_q", ctypes.c_int32),
+                ("block", ctypes.c_int32), ("scale", ctypes.c_float)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32
+        P, C = ctypes.POINTER(c_problem), ctypes.POINTER(c_head_config)
+        L.mmi_workspace_bytes.restype = sz
+        L.mmi_workspace_bytes.argtypes = [P, C]
+        L.mmi_estimate_index.argtypes = [P, C, vp, vp, vp, vp, sz, vp]
+        L.mmi_permute.argtypes = [P, C, vp, sz, vp, vp, vp, vp]
+        L.mmi_sparse_prefill.argtypes = [P, C, vp, sz, vp, vp, vp, vp, vp, vp]
+        L.mmi_unpermute.argtypes = [P, C, vp, sz, vp, vp, vp]
+        L.mmi_dense_prefill.argtypes = [P, vp, vp, vp, vp, vp, vp]
+        L.mmi_export_index.argtypes = [P, C, vp, sz, i32, vp, ctypes.POINTER(sz), vp]
+        L.mmi_sparse_fingerprint.argtypes = [P, C, vp, sz, vp, vp, vp, vp, vp]
+        L.mmi_last_error.restype = ctypes.c_char_p
+        L.mmi_version.restype = ctypes.c_char_p
+        for fn in ("mmi_estimate_index", "mmi_permute", "mmi_sparse_prefill", "mmi_unpermute",
+                   "mmi_dense_prefill", "mmi_export_index", "mmi_sparse_fingerprint"):
+            getattr(L, fn).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != MMI_OK:
+        raise MMIError(st, lib().mmi_last_error().decode())
+
+
+def to_c_pattern(p: Pattern) -> c_pattern:
+    return c_pattern(p.kind, p.sink, p.local, p.n_vertical, p.n_slash, p.stride, p.stride_min, p.stride_max,
+                     int(p.use_hline), int(p.use_vline), int(p.use_slash), 0)
+
+
+def to_c_configs(cfgs: Sequence[HeadConfig]):
+    arr = (c_head_config * len(cfgs))()
+    for i, c in enumerate(cfgs):
+        arr[i].boundary = c.boundary
+        for m in range(MAX_MOD):
+            arr[i].intra[m] = to_c_pattern(c.intra[m])
+            for b in range(MAX_MOD):
+                arr[i].pair[m][b] = to_c_pattern(c.pair[m][b])
+    return arr
+
+
+def to_c_problem(pb: Problem) -> c_problem:
+    return c_problem(pb.n_heads, pb.n_kv_heads, pb.seq_len, pb.head_dim, pb.n_modalities, pb.last_q, pb.block,
+                     float(pb.scale))
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("device tensor expected")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need_cuda(*ts):
+    if not torch.cuda.is_available():
+        raise RuntimeError("mmi: CUDA device required (no CPU fallback)")
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("mmi: contiguous CUDA tensors required")
+
+
+# ------------------------------------------------------------------ C ABI mirrors
+def mmi_workspace_bytes(pb: Problem, cfgs: Sequence[HeadConfig]) -> int:
+    return int(lib().mmi_workspace_bytes(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs)))
+
+
+def mmi_estimate_index(pb, cfgs, q, k, modality, ws, stream=None):
+    _need_cuda(q, k, modality, ws)
+    _check(lib().mmi_estimate_index(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(q), _ptr(k),
+                                    _ptr(modality), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def mmi_permute(pb, cfgs, ws, q, k, v, stream=None):
+    _need_cuda(q, k, v, ws)
+    _check(lib().mmi_permute(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
+                             ws.numel() * ws.element_size(), _ptr(q), _ptr(k), _ptr(v), _stream(stream)))
+
+
+def mmi_sparse_prefill(pb, cfgs, ws, q, k, v, o, lse=None, stream=None):
+    _need_cuda(q, k, v, o, ws, lse)
+    _check(lib().mmi_sparse_prefill(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
+                                    ws.numel() * ws.element_size(), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                                    _stream(stream)))
+
+
+def mmi_unpermute(pb, cfgs, ws, o, lse=None, stream=None):
+    _need_cuda(o, ws, lse)
+    _check(lib().mmi_unpermute(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
+                               ws.numel() * ws.element_size(), _ptr(o), _ptr(lse), _stream(stream)))
+
+
+def mmi_dense_prefill(pb, q, k, v, o, lse=None, stream=None):
+    _need_cuda(q, k, v, o, lse)
+    _check(lib().mmi_dense_prefill(ctypes.byref(to_c_problem(pb)), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                                   _stream(stream)))
+
+
+def mmi_sparse_fingerprint(pb, cfgs, ws, q, k, v, fp, stream=None):
+    _need_cuda(q, k, v, ws, fp)
+    _check(lib().mmi_sparse_fingerprint(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
+                                        ws.numel() * ws.element_size(), _ptr(q), _ptr(k), _ptr(v), _ptr(fp),
+                                        _stream(stream)))
+
+
+def mmi_export_index(pb, cfgs, ws, head: int, stream=None) -> torch.Tensor:
+    """TEST ONLY: int32 words of head `head`'s index (layout: see api.cu export)."""
+    n = ctypes.c_size_t(0)
+    c_pb, c_cfg = to_c_problem(pb), to_c_configs(cfgs)
+    sz = ws.numel() * ws.element_size()
+    _check(lib().mmi_export_index(ctypes.byref(c_pb), c_cfg, _ptr(ws), sz, head, None, ctypes.byref(n),
+                                  _stream(stream)))
+    buf = torch.zeros(int(n.value), dtype=torch.int32)
+    _check(lib().mmi_export_index(ctypes.byref(c_pb), c_cfg, _ptr(ws), sz, head,
+                                  ctypes.c_void_p(buf.data_ptr()), ctypes.byref(n), _stream(stream)))
+    return buf
+
+
+# ------------------------------------------------------------------ convenience
+class SparsePrefill:
+    """One layer's sparse pre-fill: owns the workspace, runs the four C-ABI calls."""
+
+    def __init__(self, pb: Problem, cfgs: List[HeadConfig], device="cuda"):
+        self.pb, self.cfgs = pb, list(cfgs)
+        nbytes = mmi_workspace_bytes(pb, self.cfgs)
+        if nbytes == 0:
+            raise MMIError(1, lib().mmi_last_error().decode())
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+    def __call__(self, q, k, v, modality, o=None, lse=None, stream=None):
+        pb = self.pb
+        if o is None:
+            o = torch.empty((pb.n_heads, pb.seq_len, pb.head_dim), dtype=torch.bfloat16, device=q.device)
+        mmi_estimate_index(pb, self.cfgs, q, k, modality, self.ws, stream)
+        mmi_permute(pb, self.cfgs, self.ws, q, k, v, stream)
+        mmi_sparse_prefill(pb, self.cfgs, self.ws, q, k, v, o, lse, stream)
+        mmi_unpermute(pb, self.cfgs, self.ws, o, lse, stream)
+        return o
+
+
+def dense_prefill(pb: Problem, q, k, v, o=None, lse=None, stream=None):
+    if o is None:
+        o = torch.empty((pb.n_heads, pb.seq_len, pb.head_dim), dtype=torch.bfloat16, device=q.device)
+    mmi_dense_prefill(pb, q, k, v, o, lse, stream)
+    return o
