@@ -30,6 +30,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define MMI_API __attribute__((visibility("default")))
+#else
+#define MMI_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -93,54 +99,54 @@ typedef struct {
 } mmi_problem;
 
 /* Bytes of device workspace needed for (problem, cfg_host[0..H-1]).  0 on invalid input. */
-size_t mmi_workspace_bytes(const mmi_problem* problem, const mmi_head_config* cfg_host);
+MMI_API size_t mmi_workspace_bytes(const mmi_problem* problem, const mmi_head_config* cfg_host);
 
 /* Step a1-a5: modality bookkeeping, last_q slab estimation, VS
  * top-k, grid stride/phase search and index (view + tile list) construction.
  * Reads q, k, modality; writes only the workspace. */
-mmi_status mmi_estimate_index(const mmi_problem* problem, const mmi_head_config* cfg_host,
+MMI_API mmi_status mmi_estimate_index(const mmi_problem* problem, const mmi_head_config* cfg_host,
                               const void* q, const void* k, const uint8_t* modality,
                               void* ws, size_t ws_bytes, mmi_stream_t stream);
 
 /* Step a6: gather the permuted Q̄ / K̄ / V̄ views the index needs into the
  * workspace (pads zero-filled).  Requires mmi_estimate_index on the same ws. */
-mmi_status mmi_permute(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws, size_t ws_bytes,
+MMI_API mmi_status mmi_permute(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws, size_t ws_bytes,
                        const void* q, const void* k, const void* v, mmi_stream_t stream);
 
 /* Step a7: block-sparse causal attention over every work item of the index
  * (tcgen05 / TMEM / TMA kernel).  Rows owned by a single pass are written to
  * o / lse directly; rows with several passes leave fp32 partials in ws.
  * lse may be NULL. */
-mmi_status mmi_sparse_prefill(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws,
+MMI_API mmi_status mmi_sparse_prefill(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws,
                               size_t ws_bytes, const void* q, const void* k, const void* v, void* o, float* lse,
                               mmi_stream_t stream);
 
 /* Step a8: LSE-merge the partial rows and scatter them to token order in o / lse.
  * After this call o [H,S,D] holds the complete sparse attention output. */
-mmi_status mmi_unpermute(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws, size_t ws_bytes,
+MMI_API mmi_status mmi_unpermute(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws, size_t ws_bytes,
                          void* o, float* lse, mmi_stream_t stream);
 
 /* Same-build dense causal attention (the comparator), same kernel and tiles. */
-mmi_status mmi_dense_prefill(const mmi_problem* problem, const void* q, const void* k, const void* v, void* o,
+MMI_API mmi_status mmi_dense_prefill(const mmi_problem* problem, const void* q, const void* k, const void* v, void* o,
                              float* lse, mmi_stream_t stream);
 
 /* TEST ONLY (synchronises the stream).  Copies the estimated index of head h
  * to host_buf as int32 words: see mmi_export_layout in the Python binding.
  * Returns the number of int32 words needed when host_buf is NULL (via *words). */
-mmi_status mmi_export_index(const mmi_problem* problem, const mmi_head_config* cfg_host, const void* ws,
+MMI_API mmi_status mmi_export_index(const mmi_problem* problem, const mmi_head_config* cfg_host, const void* ws,
                             size_t ws_bytes, int32_t head, int32_t* host_buf, size_t* words, mmi_stream_t stream);
 
 /* TEST ONLY: per-row admitted-key fingerprints (count, sum pos, sum pos^2) of
  * the sparse pass, int64 [H, S, 3] device buffer (zeroed by the caller). */
-mmi_status mmi_sparse_fingerprint(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws,
+MMI_API mmi_status mmi_sparse_fingerprint(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws,
                                   size_t ws_bytes, const void* q, const void* k, const void* v, int64_t* fp,
                                   mmi_stream_t stream);
 
 /* Thread-local message for the last non-OK status of this thread. */
-const char* mmi_last_error(void);
+MMI_API const char* mmi_last_error(void);
 
 /* Library version string. */
-const char* mmi_version(void);
+MMI_API const char* mmi_version(void);
 
 #ifdef __cplusplus
 }

@@ -5,11 +5,20 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
 
 #include "../../include/mmi.h"
+#include "estimate.h"
+#include "index.h"
 #include "internal.h"
+#include "plan.h"
 
-static thread_local char g_err[512];
+using namespace mmi;
+
+static thread_local char g_err[1024];
 
 static mmi_status fail(mmi_status st, const char* fmt, ...) {
   va_list ap;
@@ -19,12 +28,8 @@ static mmi_status fail(mmi_status st, const char* fmt, ...) {
   return st;
 }
 
-namespace mmi {
-mmi_status set_error(mmi_status st, const char* msg) { return fail(st, "%s", msg); }
-}  // namespace mmi
-
 extern "C" const char* mmi_last_error(void) { return g_err; }
-extern "C" const char* mmi_version(void) { return "mmi-b200 0.1 (sm_100a)"; }
+extern "C" const char* mmi_version(void) { return "mmi-b200 0.2 (sm_100a)"; }
 
 static mmi_status check_problem(const mmi_problem* pb) {
   if (!pb) return fail(MMI_E_INVALID, "problem is NULL");
@@ -33,7 +38,7 @@ static mmi_status check_problem(const mmi_problem* pb) {
                 pb->n_kv_heads);
   if (pb->head_dim != 64 && pb->head_dim != 128) return fail(MMI_E_SHAPE, "head_dim %d not in {64,128}", pb->head_dim);
   if (pb->seq_len < 1) return fail(MMI_E_SHAPE, "seq_len %d < 1", pb->seq_len);
-  if ((long long)pb->seq_len * pb->n_heads > (1ll << 31) / 2)
+  if ((long long)(pb->seq_len + 4 * 128) * pb->n_heads > (1ll << 30))
     return fail(MMI_E_UNSUPPORTED, "H*S too large for 32-bit row indexing");
   if (pb->block != 128) return fail(MMI_E_UNSUPPORTED, "block must be 128");
   if (pb->n_modalities < 1 || pb->n_modalities > MMI_MAX_MOD)
@@ -46,22 +51,263 @@ static float tau_of(const mmi_problem* pb) {
   return pb->scale > 0.f ? pb->scale : 1.0f / sqrtf((float)pb->head_dim);
 }
 
+static mmi_status prepare(const mmi_problem* pb, const mmi_head_config* cfg, const void* ws, size_t ws_bytes,
+                          Plan& P, bool need_ws = true) {
+  mmi_status st = check_problem(pb);
+  if (st != MMI_OK) return st;
+  std::string err;
+  st = build_plan(pb, cfg, P, err);
+  if (st != MMI_OK) return fail(st, "%s", err.c_str());
+  if (need_ws) {
+    if (!ws) return fail(MMI_E_WORKSPACE, "workspace is NULL");
+    if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(MMI_E_WORKSPACE, "workspace not 256-byte aligned");
+    if (ws_bytes < P.total)
+      return fail(MMI_E_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, P.total);
+  }
+  return MMI_OK;
+}
+
+template <typename T>
+static T* at(void* ws, const Region& r) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + r.off);
+}
+template <typename T>
+static T* blob_at(void* ws, const Plan& P, size_t sub) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + P.blob.off + sub);
+}
+
+static IndexCtx make_ctx(const Plan& P, void* ws) {
+  IndexCtx C;
+  memset(&C, 0, sizeof(C));
+  C.S = P.S;
+  C.H = P.H;
+  C.M = P.M;
+  C.n_slots = P.n_slots;
+  C.n_passes = (int)P.passes.size();
+  C.heads = blob_at<DHead>(ws, P, P.o_heads);
+  C.insts = blob_at<DInst>(ws, P, P.o_insts);
+  C.views = blob_at<DView>(ws, P, P.o_views);
+  C.passes = blob_at<DPass>(ws, P, P.o_passes);
+  C.info = at<int>(ws, P.mod_cnt);
+  C.perm = at<int>(ws, P.perm);
+  C.rank = at<int>(ws, P.rank);
+  C.modpos = at<int>(ws, P.modpos);
+  C.labels = at<uint8_t>(ws, P.labels);
+  C.gridres = at<GridRes>(ws, P.gridres);
+  C.vs_lists = at<int>(ws, P.vs_lists);
+  C.vs_cnt = at<int>(ws, P.vs_cnt);
+  C.vs_list_off = blob_at<int64_t>(ws, P, P.o_vsl);
+  C.vs_bits_off = blob_at<int64_t>(ws, P, P.o_vsb);
+  C.view_len = at<int>(ws, P.view_len);
+  C.qg_pos = at<int>(ws, P.qg_pos);
+  C.qg_rank = at<int>(ws, P.qg_rank);
+  C.qg_src = at<int>(ws, P.qg_src);
+  C.kg_pos = at<int>(ws, P.kg_pos);
+  C.kg_rank = at<int>(ws, P.kg_rank);
+  C.kg_src = at<int>(ws, P.kg_src);
+  C.inst_params = at<InstParam>(ws, P.inst_params);
+  C.seg_cnt = at<int>(ws, P.seg_cnt);
+  C.seg_off = at<int>(ws, P.seg_off);
+  C.segs = at<Seg>(ws, P.segs);
+  C.items = at<WorkItem>(ws, P.items);
+  C.items_sorted = at<WorkItem>(ws, P.items_sorted);
+  C.sort_keys = at<int>(ws, P.item_keys);
+  C.sort_vals = at<int>(ws, P.item_vals);
+  C.sort_vals_out = at<int>(ws, P.item_vals) + P.n_slots;
+  C.part_o = at<float>(ws, P.part_o);
+  C.part_lse = at<float>(ws, P.part_lse);
+  return C;
+}
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t _e = (x);                                                                  \
+    if (_e != cudaSuccess) return fail(MMI_E_CUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
+  } while (0)
+
+extern "C" size_t mmi_workspace_bytes(const mmi_problem* pb, const mmi_head_config* cfg) {
+  Plan P;
+  if (prepare(pb, cfg, nullptr, 0, P, false) != MMI_OK) return 0;
+  return P.total;
+}
+
+extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_config* cfg, const void* q,
+                                         const void* k, const uint8_t* modality, void* ws, size_t ws_bytes,
+                                         mmi_stream_t stream) {
+  Plan P;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  if (st != MMI_OK) return st;
+  if (!q || !k || !modality) return fail(MMI_E_INVALID, "null tensor pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int S = P.S;
+  // device tables (pageable source: staged before cudaMemcpyAsync returns)
+  std::vector<uint8_t> blob = make_blob(P);
+  CK(cudaMemcpyAsync(at<char>(ws, P.blob), blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(at<uint8_t>(ws, P.labels), modality, S, cudaMemcpyDeviceToDevice, s));
+  // zero the accumulators
+  CK(cudaMemsetAsync(at<char>(ws, P.cbuf), 0, P.cbuf.bytes, s));
+  CK(cudaMemsetAsync(at<char>(ws, P.dgbuf), 0, P.dgbuf.bytes, s));
+  CK(cudaMemsetAsync(at<char>(ws, P.bits), 0, P.bits.bytes, s));
+  CK(cudaMemsetAsync(at<char>(ws, P.vs_cnt), 0, P.vs_cnt.bytes, s));
+  CK(cudaMemsetAsync(at<char>(ws, P.seg_cnt), 0, P.seg_cnt.bytes, s));
+  const int64_t mod_cap = (P.S + (int64_t)P.M * BLK + BLK - 1) / BLK * BLK;
+  IndexCtx C = make_ctx(P, ws);
+  int* info = at<int>(ws, P.mod_cnt);
+  const int nch = (S + 4095) / 4096;
+  int* chunk_cnt = at<int>(ws, P.mod_off);
+  int* chunk_base = chunk_cnt + (size_t)nch * MAX_MOD;
+  // a1 modality bookkeeping
+  launch_modality(at<uint8_t>(ws, P.labels), S, P.M, P.S_pad, (int)mod_cap, chunk_cnt, chunk_base, info,
+                  at<int>(ws, P.perm), at<int>(ws, P.rank), at<int>(ws, P.modpos), s);
+  // a2 last_q slab estimation
+  int* srows = at<int>(ws, P.slab_rows);
+  const size_t ns = std::max<size_t>(P.slabs.size(), 1);
+  int* srank = srows + ns * SLAB_ROWS;
+  int* sinfo = srank + ns * SLAB_ROWS;
+  const DSlab* dslabs = blob_at<DSlab>(ws, P, P.o_slabs);
+  launch_slabs(dslabs, (int)P.slabs.size(), q, k, S, P.H, P.Hkv, P.D, P.pb.last_q, tau_of(pb) * 1.4426950408889634f,
+               info, at<int>(ws, P.perm), at<int>(ws, P.rank), at<uint8_t>(ws, P.labels), srows, srank, sinfo,
+               at<float2>(ws, P.slab_ml_part), at<float2>(ws, P.slab_ml), at<float>(ws, P.cbuf),
+               at<unsigned long long>(ws, P.dgbuf), P.n_chunks, s);
+  // a3 grid stride / phase
+  const DInst* dinsts = blob_at<DInst>(ws, P, P.o_insts);
+  launch_grid(dinsts, blob_at<int>(ws, P, P.o_gi), P.n_grid, P.max_ncand, (int)P.insts.size(), dslabs, sinfo, info,
+              at<int>(ws, P.perm), at<float>(ws, P.cbuf), at<float>(ws, P.c_rank), S, P.S_pad,
+              at<GridRes>(ws, P.gridres), at<double>(ws, P.grid_part), s);
+  // a4 vertical-slash top-k
+  launch_vs(dinsts, blob_at<int>(ws, P, P.o_vi), P.n_vs, dslabs, sinfo, info, at<int>(ws, P.perm),
+            at<float>(ws, P.cbuf), at<unsigned long long>(ws, P.dgbuf), blob_at<int64_t>(ws, P, P.o_vsl),
+            blob_at<int64_t>(ws, P, P.o_vsb), at<int>(ws, P.vs_lists), at<int>(ws, P.vs_cnt),
+            at<uint32_t>(ws, P.bits), s);
+  // a5 views, instance parameters, work items (count -> scan -> fill -> LPT sort)
+  launch_build_views(C, blob_at<int>(ws, P, P.o_qv), (int)P.qview_ids.size(), blob_at<int>(ws, P, P.o_kv),
+                     (int)P.kview_ids.size(), P.qg_rows, P.kg_rows, s);
+  launch_inst_params(C, (int)P.insts.size(), s);
+  launch_items_count(C, s);
+  size_t tb = P.scan_tmp_bytes;
+  CK(cub::DeviceScan::ExclusiveSum(at<char>(ws, P.scan_tmp), tb, C.seg_cnt, (int*)C.seg_off, P.n_slots + 1, s));
+  launch_items_fill(C, s);
+  tb = P.sort_tmp_bytes;
+  CK(cub::DeviceRadixSort::SortPairsDescending(at<char>(ws, P.sort_tmp), tb, C.sort_keys, C.sort_keys + P.n_slots,
+                                               C.sort_vals, (int*)C.sort_vals_out, P.n_slots, 0, 32, s));
+  launch_items_gather(C, s);
+  CK(cudaGetLastError());
+  return MMI_OK;
+}
+
+extern "C" mmi_status mmi_permute(const mmi_problem* pb, const mmi_head_config* cfg, void* ws, size_t ws_bytes,
+                                  const void* q, const void* k, const void* v, mmi_stream_t stream) {
+  Plan P;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  if (st != MMI_OK) return st;
+  if (!q || !k || !v) return fail(MMI_E_INVALID, "null tensor pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_gather(at<int>(ws, P.qg_src), P.qg_rows, P.D, q, at<void>(ws, P.qg), nullptr, nullptr, s);
+  launch_gather(at<int>(ws, P.kg_src), P.kg_rows, P.D, k, at<void>(ws, P.kg), v, at<void>(ws, P.vg), s);
+  CK(cudaGetLastError());
+  return MMI_OK;
+}
+
+static mmi_status run_sparse(const Plan& P, const mmi_problem* pb, void* ws, const void* q, const void* k,
+                             const void* v, void* o, float* lse, int64_t* fp, cudaStream_t s) {
+  AttnParams A;
+  memset(&A, 0, sizeof(A));
+  A.items = at<WorkItem>(ws, P.items_sorted);
+  A.n_items = P.n_slots;
+  A.segs = at<Seg>(ws, P.segs);
+  A.insts = at<InstParam>(ws, P.inst_params);
+  A.bits = at<uint32_t>(ws, P.bits);
+  A.qg_pos = at<int>(ws, P.qg_pos);
+  A.qg_rank = at<int>(ws, P.qg_rank);
+  A.kg_pos = at<int>(ws, P.kg_pos);
+  A.kg_rank = at<int>(ws, P.kg_rank);
+  A.rank = at<int>(ws, P.rank);
+  A.labels = at<uint8_t>(ws, P.labels);
+  A.o = o;
+  A.lse = lse;
+  A.part_o = at<float>(ws, P.part_o);
+  A.part_lse = at<float>(ws, P.part_lse);
+  A.S = P.S;
+  A.H = P.H;
+  A.Hkv = P.Hkv;
+  A.D = P.D;
+  A.scale_log2 = tau_of(pb) * 1.4426950408889634f;
+  A.dense = 0;
+  A.fingerprint = fp ? 1 : 0;
+  A.fp_out = fp;
+  AttnLaunch L;
+  L.q = q;
+  L.qg = at<void>(ws, P.qg);
+  L.k = k;
+  L.kg = at<void>(ws, P.kg);
+  L.v = v;
+  L.vg = at<void>(ws, P.vg);
+  L.q_rows = (long long)P.H * P.S;
+  L.qg_rows = P.qg_rows;
+  L.kv_rows = (long long)P.Hkv * P.S;
+  L.kvg_rows = P.kg_rows;
+  int te = 0;
+  cudaError_t e = launch_attn(L, A, P.n_slots, s, &te);
+  if (te) return fail(MMI_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", te);
+  if (e != cudaSuccess) return fail(MMI_E_CUDA, "attention launch: %s", cudaGetErrorString(e));
+  return MMI_OK;
+}
+
+extern "C" mmi_status mmi_sparse_prefill(const mmi_problem* pb, const mmi_head_config* cfg, void* ws,
+                                         size_t ws_bytes, const void* q, const void* k, const void* v, void* o,
+                                         float* lse, mmi_stream_t stream) {
+  Plan P;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  if (st != MMI_OK) return st;
+  if (!q || !k || !v || !o) return fail(MMI_E_INVALID, "null tensor pointer");
+  return run_sparse(P, pb, ws, q, k, v, o, lse, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" mmi_status mmi_sparse_fingerprint(const mmi_problem* pb, const mmi_head_config* cfg, void* ws,
+                                             size_t ws_bytes, const void* q, const void* k, const void* v,
+                                             int64_t* fp, mmi_stream_t stream) {
+  Plan P;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  if (st != MMI_OK) return st;
+  if (!q || !k || !v || !fp) return fail(MMI_E_INVALID, "null tensor pointer");
+  return run_sparse(P, pb, ws, q, k, v, nullptr, nullptr, fp, (cudaStream_t)stream);
+}
+
+extern "C" mmi_status mmi_unpermute(const mmi_problem* pb, const mmi_head_config* cfg, void* ws, size_t ws_bytes,
+                                    void* o, float* lse, mmi_stream_t stream) {
+  Plan P;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  if (st != MMI_OK) return st;
+  if (!o) return fail(MMI_E_INVALID, "null output pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  IndexCtx C = make_ctx(P, ws);
+  const int64_t mod_cap = (P.S + (int64_t)P.M * BLK + BLK - 1) / BLK * BLK;
+  for (int h = 0; h < P.H; ++h) {
+    const DHead& hd = P.heads[h];
+    if (hd.part_rows0 < 0) continue;
+    const int rows = hd.qmod_view >= 0 ? (int)mod_cap : P.nb * BLK;
+    launch_merge(C, P.D, h, rows, o, lse, s);
+  }
+  CK(cudaGetLastError());
+  return MMI_OK;
+}
+
 extern "C" mmi_status mmi_dense_prefill(const mmi_problem* pb, const void* q, const void* k, const void* v, void* o,
                                         float* lse, mmi_stream_t stream) {
   mmi_status st = check_problem(pb);
   if (st != MMI_OK) return st;
   if (!q || !k || !v || !o) return fail(MMI_E_INVALID, "null tensor pointer");
-  mmi::AttnParams P;
-  memset(&P, 0, sizeof(P));
-  P.S = pb->seq_len;
-  P.H = pb->n_heads;
-  P.Hkv = pb->n_kv_heads;
-  P.D = pb->head_dim;
-  P.scale_log2 = tau_of(pb) * 1.4426950408889634f;
-  P.dense = 1;
-  P.o = o;
-  P.lse = lse;
-  mmi::AttnLaunch L;
+  AttnParams A;
+  memset(&A, 0, sizeof(A));
+  A.S = pb->seq_len;
+  A.H = pb->n_heads;
+  A.Hkv = pb->n_kv_heads;
+  A.D = pb->head_dim;
+  A.scale_log2 = tau_of(pb) * 1.4426950408889634f;
+  A.dense = 1;
+  A.o = o;
+  A.lse = lse;
+  AttnLaunch L;
   memset(&L, 0, sizeof(L));
   L.q = q;
   L.k = k;
@@ -70,35 +316,96 @@ extern "C" mmi_status mmi_dense_prefill(const mmi_problem* pb, const void* q, co
   L.kv_rows = (long long)pb->n_kv_heads * pb->seq_len;
   int te = 0;
   const int nb = (pb->seq_len + 127) / 128;
-  cudaError_t e = mmi::launch_attn(L, P, pb->n_heads * nb, (cudaStream_t)stream, &te);
+  cudaError_t e = launch_attn(L, A, pb->n_heads * nb, (cudaStream_t)stream, &te);
   if (te) return fail(MMI_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", te);
   if (e != cudaSuccess) return fail(MMI_E_CUDA, "attention launch: %s", cudaGetErrorString(e));
   return MMI_OK;
 }
 
-// ---- temporary stubs (replaced as the sparse path lands) ----
-extern "C" size_t mmi_workspace_bytes(const mmi_problem*, const mmi_head_config*) { return 0; }
-extern "C" mmi_status mmi_estimate_index(const mmi_problem*, const mmi_head_config*, const void*, const void*,
-                                         const uint8_t*, void*, size_t, mmi_stream_t) {
-  return fail(MMI_E_UNSUPPORTED, "not yet");
-}
-extern "C" mmi_status mmi_permute(const mmi_problem*, const mmi_head_config*, void*, size_t, const void*,
-                                  const void*, const void*, mmi_stream_t) {
-  return fail(MMI_E_UNSUPPORTED, "not yet");
-}
-extern "C" mmi_status mmi_sparse_prefill(const mmi_problem*, const mmi_head_config*, void*, size_t, const void*,
-                                         const void*, const void*, void*, float*, mmi_stream_t) {
-  return fail(MMI_E_UNSUPPORTED, "not yet");
-}
-extern "C" mmi_status mmi_unpermute(const mmi_problem*, const mmi_head_config*, void*, size_t, void*, float*,
-                                    mmi_stream_t) {
-  return fail(MMI_E_UNSUPPORTED, "not yet");
-}
-extern "C" mmi_status mmi_export_index(const mmi_problem*, const mmi_head_config*, const void*, size_t, int32_t,
-                                       int32_t*, size_t*, mmi_stream_t) {
-  return fail(MMI_E_UNSUPPORTED, "not yet");
-}
-extern "C" mmi_status mmi_sparse_fingerprint(const mmi_problem*, const mmi_head_config*, void*, size_t,
-                                             const void*, const void*, const void*, int64_t*, mmi_stream_t) {
-  return fail(MMI_E_UNSUPPORTED, "not yet");
+// Export layout (int32 words), for head h:
+//   [0] n_inst
+//   per instance: kind, qa, kb, rank, s, p, valid, J (2 words, double bits), nV, nS, V[nV], Sl[nS]
+//   then: items with tiles, total tiles (2 words, int64), segments
+extern "C" mmi_status mmi_export_index(const mmi_problem* pb, const mmi_head_config* cfg, const void* ws,
+                                       size_t ws_bytes, int32_t head, int32_t* host_buf, size_t* words,
+                                       mmi_stream_t stream) {
+  Plan P;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  if (st != MMI_OK) return st;
+  if (head < 0 || head >= P.H) return fail(MMI_E_INVALID, "head out of range");
+  if (!words) return fail(MMI_E_INVALID, "words is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaStreamSynchronize(s));
+  void* w = const_cast<void*>(ws);
+  std::vector<GridRes> gr(std::max(P.n_grid, 1));
+  std::vector<int> cnt(2 * std::max(P.n_vs, 1));
+  CK(cudaMemcpy(gr.data(), at<GridRes>(w, P.gridres), sizeof(GridRes) * gr.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cnt.data(), at<int>(w, P.vs_cnt), sizeof(int) * cnt.size(), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> out;
+  const DHead& hd = P.heads[head];
+  out.push_back(hd.n_inst);
+  for (int i = 0; i < hd.n_inst; ++i) {
+    const DInst& x = P.insts[(size_t)head * MAX_INST + i];
+    out.push_back(x.kind);
+    out.push_back(x.qa);
+    out.push_back(x.kb);
+    out.push_back(x.rank);
+    int32_t gs = 0, gp = 0, gv = 0;
+    double J = 0;
+    if (x.grid_id >= 0) {
+      gs = gr[x.grid_id].s;
+      gp = gr[x.grid_id].p;
+      gv = gr[x.grid_id].valid;
+      J = gr[x.grid_id].J;
+    }
+    out.push_back(gs);
+    out.push_back(gp);
+    out.push_back(gv);
+    int32_t jw[2];
+    memcpy(jw, &J, 8);
+    out.push_back(jw[0]);
+    out.push_back(jw[1]);
+    int nV = 0, nS = 0;
+    std::vector<int> V, Sl;
+    if (x.vs_id >= 0) {
+      nV = cnt[2 * x.vs_id];
+      nS = cnt[2 * x.vs_id + 1];
+      V.resize(nV);
+      Sl.resize(nS);
+      if (nV)
+        CK(cudaMemcpy(V.data(), at<int>(w, P.vs_lists) + P.vs_v_off[x.vs_id], sizeof(int) * nV,
+                      cudaMemcpyDeviceToHost));
+      if (nS)
+        CK(cudaMemcpy(Sl.data(), at<int>(w, P.vs_lists) + P.vs_s_off[x.vs_id], sizeof(int) * nS,
+                      cudaMemcpyDeviceToHost));
+    }
+    out.push_back(nV);
+    out.push_back(nS);
+    out.insert(out.end(), V.begin(), V.end());
+    out.insert(out.end(), Sl.begin(), Sl.end());
+  }
+  std::vector<WorkItem> items(P.n_slots);
+  CK(cudaMemcpy(items.data(), at<WorkItem>(w, P.items), sizeof(WorkItem) * P.n_slots, cudaMemcpyDeviceToHost));
+  int n_it = 0, n_seg = 0;
+  long long tiles = 0;
+  for (const auto& it : items)
+    if (it.head == head && it.n_tiles > 0) {
+      ++n_it;
+      tiles += it.n_tiles;
+      n_seg += it.n_segs;
+    }
+  out.push_back(n_it);
+  int32_t tw[2];
+  memcpy(tw, &tiles, 8);
+  out.push_back(tw[0]);
+  out.push_back(tw[1]);
+  out.push_back(n_seg);
+  if (!host_buf) {
+    *words = out.size();
+    return MMI_OK;
+  }
+  if (*words < out.size()) return fail(MMI_E_INVALID, "host_buf too small (%zu < %zu words)", *words, out.size());
+  memcpy(host_buf, out.data(), sizeof(int32_t) * out.size());
+  *words = out.size();
+  return MMI_OK;
 }

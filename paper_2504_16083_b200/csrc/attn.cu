@@ -52,7 +52,8 @@ struct Smem {
 };
 
 struct ItemView {
-  int head, q_row0, tile_off, n_tiles, q_gathered, out_mode, out_row0, inst_base, skip_s, skip_p, skip_rank;
+  int head, q_row0, seg_off, n_segs, n_tiles, q_gathered, out_mode, out_row0, inst_base, skip_s, skip_p, skip_rank,
+      row_mod, rb;
 };
 
 __device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx) {
@@ -62,7 +63,9 @@ __device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx) {
     const int rb = nb - 1 - idx / P.H;  // longest rows first (LPT)
     v.head = idx % P.H;
     v.q_row0 = v.head * P.S + rb * BLK;
-    v.tile_off = rb;  // reused: row block index
+    v.rb = rb;
+    v.seg_off = 0;
+    v.n_segs = 1;
     v.n_tiles = rb + 1;
     v.q_gathered = 0;
     v.out_mode = OUT_FINAL;
@@ -71,12 +74,14 @@ __device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx) {
     v.skip_s = 0;
     v.skip_p = 0;
     v.skip_rank = 0;
+    v.row_mod = -1;
     return v;
   }
   const WorkItem w = P.items[idx];
   v.head = w.head;
   v.q_row0 = w.q_row0;
-  v.tile_off = w.tile_off;
+  v.seg_off = w.seg_off;
+  v.n_segs = w.n_segs;
   v.n_tiles = w.n_tiles;
   v.q_gathered = w.q_gathered;
   v.out_mode = w.out_mode;
@@ -85,19 +90,51 @@ __device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx) {
   v.skip_s = w.skip_s;
   v.skip_p = w.skip_p;
   v.skip_rank = w.skip_rank;
+  v.row_mod = w.row_mod;
+  v.rb = 0;
   return v;
 }
 
-__device__ __forceinline__ TileEnt load_tile(const AttnParams& P, const ItemView& it, int t) {
-  if (P.dense) {
-    const int kv = it.head / (P.H / P.Hkv);
-    TileEnt e;
-    e.krow = kv * P.S + t * BLK;
-    e.meta = tile_meta(0, t == it.tile_off ? 1u : 0u, R_TRUE, 0, 0);
-    return e;
+struct TileInfo {
+  int krow;
+  uint32_t space, pred, role, rmode, inst;
+};
+
+// walks the item's segments tile by tile (every warp role keeps its own cursor)
+struct SegIter {
+  Seg cur;
+  int seg_i, t;
+  __device__ __forceinline__ void init(const AttnParams& P, const ItemView& it) {
+    seg_i = 0;
+    t = 0;
+    if (P.dense) {
+      cur.krow0 = (it.head / (P.H / P.Hkv)) * P.S;
+      cur.ntiles = it.rb + 1;
+      cur.meta = seg_meta(0, R_TRUE, 0, 0);
+      cur.pred_head = 0;
+      cur.pred_tail = 1;
+    } else {
+      cur.ntiles = 0;
+      seg_i = -1;
+    }
   }
-  return P.tiles[it.tile_off + t];
-}
+  __device__ __forceinline__ TileInfo next(const AttnParams& P, const ItemView& it) {
+    while (t >= cur.ntiles) {
+      ++seg_i;
+      cur = P.segs[it.seg_off + seg_i];
+      t = 0;
+    }
+    TileInfo ti;
+    ti.krow = cur.krow0 + t * BLK;
+    ti.space = cur.meta & 1u;
+    ti.role = (cur.meta >> 2) & 7u;
+    ti.rmode = (cur.meta >> 5) & 1u;
+    ti.inst = (cur.meta >> 8) & 0xffu;
+    ti.pred = (t < cur.pred_head || t >= cur.ntiles - cur.pred_tail) ? 1u : 0u;
+    ++t;
+    return ti;
+  }
+};
 
 template <int D>
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -176,9 +213,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
           tma_load_2d(smem + L::OFF_Q + c * (BLK * 128), tq, q_full, c * 64, it.q_row0);
+        SegIter si;
+        si.init(P, it);
         for (int t = 0; t < it.n_tiles; ++t) {
-          const TileEnt e = load_tile(P, it, t);
-          const uint32_t space = e.meta & 1u, pred = (e.meta >> 1) & 1u, rank = (e.meta >> 5) & 1u;
+          const TileInfo e = si.next(P, it);
+          const uint32_t space = e.space, pred = e.pred, rank = e.rmode;
           mbar_wait(kv_empty + stage, kv_phase ^ 1);
           uint32_t bytes = 2 * L::KV_BYTES;
           const bool cp_pos = (pred || P.fingerprint) && space;
@@ -288,6 +327,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int G = P.H / P.Hkv;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const ItemView it = load_item(P, idx);
+      if (it.n_tiles <= 0) continue;  // empty slot: nothing to compute or write
       // row identity
       int xpos, xrank;
       if (it.q_gathered) {
@@ -297,7 +337,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         xpos = it.q_row0 - it.head * P.S + row;
         xrank = (xpos < P.S && P.rank) ? P.rank[xpos] : xpos;
       }
-      const bool valid = xpos >= 0 && xpos < P.S;
+      bool valid = xpos >= 0 && xpos < P.S;
+      if (valid && it.row_mod >= 0) valid = (P.labels[xpos] == it.row_mod);
       bool write = valid;
       if (it.skip_s > 0 && valid) {
         const int c = it.skip_rank ? xrank : xpos;
@@ -306,10 +347,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       float m_used = -INFINITY, l_sum = 0.f;
       long long fp_cnt = 0, fp_s1 = 0, fp_s2 = 0;
       const int kv = it.head / G;
+      SegIter si;
+      si.init(P, it);
       for (int t = 0; t < it.n_tiles; ++t) {
-        const TileEnt e = load_tile(P, it, t);
-        const uint32_t space = e.meta & 1u, pred = (e.meta >> 1) & 1u, role = (e.meta >> 2) & 7u,
-                       rmode = (e.meta >> 5) & 1u, inst = (e.meta >> 8) & 0xffu;
+        const TileInfo e = si.next(P, it);
+        const uint32_t space = e.space, pred = e.pred, role = e.role, rmode = e.rmode, inst = e.inst;
         mbar_wait(s_full + sbuf, s_phase[sbuf]);
         s_phase[sbuf] ^= 1;
         tc_fence_after();

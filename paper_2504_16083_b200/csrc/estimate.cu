@@ -1,0 +1,762 @@
+// Online sparse-index estimation:
+//   a1 modality bookkeeping   (Alg.2, Alg.3: permute by modality)
+//   a2 last_q slab estimate    (Alg.1): A-hat rows, column mass c,
+//                              diagonal mass dg (fixed-point, order-independent sums)
+//   a3 grid stride/phase fold  (Alg.1, readings C4-C7)
+//   a4 vertical-slash top-k    (reading C15): radix select, ties -> lowest index
+// All reductions are deterministic (fixed order or integer atomics).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+
+#include <cub/cub.cuh>
+
+#include "estimate.h"
+
+namespace mmi {
+
+// =============================================================== a1: modality
+constexpr int MOD_CHUNK = 4096;
+
+__global__ void mod_count_kernel(const uint8_t* __restrict__ labels, int S, int M, int* __restrict__ chunk_cnt) {
+  __shared__ int cnt[MAX_MOD];
+  if (threadIdx.x < MAX_MOD) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int c0 = blockIdx.x * MOD_CHUNK;
+  int loc[MAX_MOD] = {0, 0, 0, 0};
+  for (int i = c0 + threadIdx.x; i < min(S, c0 + MOD_CHUNK); i += blockDim.x) {
+    const int m = labels[i];
+#pragma unroll
+    for (int q = 0; q < MAX_MOD; ++q) loc[q] += (m == q);
+  }
+#pragma unroll
+  for (int q = 0; q < MAX_MOD; ++q)
+    if (loc[q]) atomicAdd(&cnt[q], loc[q]);
+  __syncthreads();
+  if (threadIdx.x < MAX_MOD) chunk_cnt[blockIdx.x * MAX_MOD + threadIdx.x] = cnt[threadIdx.x];
+}
+
+// single warp: per modality sequential scan over chunks (fixed order)
+__global__ void mod_scan_kernel(const int* __restrict__ chunk_cnt, int n_chunks, int M, int* __restrict__ chunk_base,
+                                int* __restrict__ info) {
+  const int m = threadIdx.x;
+  if (m < MAX_MOD) {
+    int run = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      chunk_base[c * MAX_MOD + m] = run;
+      run += chunk_cnt[c * MAX_MOD + m];
+    }
+    info[MI_CNT + m] = (m < M) ? run : 0;
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    int o = 0, po = 0;
+    for (int q = 0; q < MAX_MOD; ++q) {
+      info[MI_OFF + q] = o;
+      info[MI_PADOFF + q] = po;
+      o += info[MI_CNT + q];
+      po += (info[MI_CNT + q] + BLK - 1) / BLK * BLK;
+    }
+    info[MI_OFF + MAX_MOD] = o;
+    info[MI_PADOFF + MAX_MOD] = po;
+  }
+}
+
+__global__ void mod_place_kernel(const uint8_t* __restrict__ labels, int S, const int* __restrict__ chunk_base,
+                                 const int* __restrict__ info, int* __restrict__ perm, int* __restrict__ rank,
+                                 int* __restrict__ modpos) {
+  // 256 threads x 16 consecutive positions = one 4096 chunk
+  typedef cub::BlockScan<int, 256> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  const int c0 = blockIdx.x * MOD_CHUNK + threadIdx.x * 16;
+  int lab[16];
+  int loc[MAX_MOD] = {0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    lab[i] = (c0 + i < S) ? labels[c0 + i] : -1;
+#pragma unroll
+    for (int q = 0; q < MAX_MOD; ++q) loc[q] += (lab[i] == q);
+  }
+  int pre[MAX_MOD];
+#pragma unroll
+  for (int q = 0; q < MAX_MOD; ++q) {
+    Scan(tmp).ExclusiveSum(loc[q], pre[q]);
+    __syncthreads();
+    pre[q] += chunk_base[blockIdx.x * MAX_MOD + q];
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int m = lab[i];
+    if (m < 0) continue;
+    int r = 0;
+#pragma unroll
+    for (int q = 0; q < MAX_MOD; ++q)
+      if (q == m) r = pre[q]++;
+    const int pos = c0 + i;
+    rank[pos] = r;
+    perm[info[MI_OFF + m] + r] = pos;
+    modpos[info[MI_PADOFF + m] + r] = pos;
+  }
+}
+
+__global__ void mod_pad_kernel(const int* __restrict__ info, int S, int S_pad, int mod_cap, int* __restrict__ rank,
+                               int* __restrict__ modpos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S && i < S_pad) rank[i] = INT_MAX / 2;
+  if (i < mod_cap) {
+    bool pad = i >= info[MI_PADOFF + MAX_MOD];
+    for (int q = 0; q < MAX_MOD; ++q)
+      if (i >= info[MI_PADOFF + q] + info[MI_CNT + q] && i < info[MI_PADOFF + q + 1]) pad = true;
+    if (pad) modpos[i] = -1;
+  }
+}
+
+void launch_modality(const uint8_t* labels, int S, int M, int S_pad, int mod_cap, int* chunk_cnt, int* chunk_base,
+                     int* info, int* perm, int* rank, int* modpos, cudaStream_t st) {
+  const int nch = (S + MOD_CHUNK - 1) / MOD_CHUNK;
+  mod_count_kernel<<<nch, 256, 0, st>>>(labels, S, M, chunk_cnt);
+  mod_scan_kernel<<<1, 32, 0, st>>>(chunk_cnt, nch, M, chunk_base, info);
+  mod_place_kernel<<<nch, 256, 0, st>>>(labels, S, chunk_base, info, perm, rank, modpos);
+  const int n = max(S_pad, mod_cap);
+  mod_pad_kernel<<<(n + 255) / 256, 256, 0, st>>>(info, S, S_pad, mod_cap, rank, modpos);
+}
+
+// =============================================================== a2: slabs
+// slab_info[s*4 + {0,1,2,3}] = {L, min pos, max pos, min rank}
+__global__ void slab_rows_kernel(const DSlab* __restrict__ slabs, int S, int last_q, const int* __restrict__ info,
+                                 const int* __restrict__ perm, const int* __restrict__ rank, int* __restrict__ rows,
+                                 int* __restrict__ rranks, int* __restrict__ sinfo) {
+  const int s = blockIdx.x, r = threadIdx.x;  // 64 threads
+  const DSlab sl = slabs[s];
+  int n, L, pos = -1;
+  if (sl.qmod < 0) {
+    n = S;
+    L = min(last_q, n);
+    if (r < L) pos = S - L + r;
+  } else {
+    n = info[MI_CNT + sl.qmod];
+    L = min(last_q, n);
+    if (r < L) pos = perm[info[MI_OFF + sl.qmod] + n - L + r];
+  }
+  rows[s * SLAB_ROWS + r] = pos;
+  rranks[s * SLAB_ROWS + r] = pos >= 0 ? rank[pos] : -1;
+  if (r == 0) {
+    sinfo[s * 4 + 0] = L;
+    sinfo[s * 4 + 1] = L > 0 ? ((sl.qmod < 0) ? S - L : perm[info[MI_OFF + sl.qmod] + n - L]) : 0;
+  }
+  if (r == L - 1) {
+    sinfo[s * 4 + 2] = pos;
+    sinfo[s * 4 + 3] = rank[(sl.qmod < 0) ? S - L : perm[info[MI_OFF + sl.qmod] + n - L]];
+  }
+  if (L == 0 && r == 0) {
+    sinfo[s * 4 + 2] = -1;
+    sinfo[s * 4 + 3] = 0;
+  }
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int D>
+struct SlabSmem {
+  static constexpr int LD = D + 8;
+  __nv_bfloat16 q[SLAB_ROWS * LD];
+  __nv_bfloat16 k[BLK * LD];
+  float a[SLAB_ROWS][BLK + 1];
+  int colidx[BLK];
+  int red[8];
+};
+
+// scores for one (slab, key tile): warp w holds rows 16w..16w+15, acc[nt][.] per mma layout
+template <int D>
+__device__ __forceinline__ void slab_tile_scores(const SlabSmem<D>& sm, float (&acc)[16][4]) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int LD = SlabSmem<D>::LD;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+    uint32_t a[4];
+    ldsm_x4(a, &sm.q[(warp * 16 + (lane % 16)) * LD + kk * 16 + (lane / 16) * 8]);
+#pragma unroll
+    for (int n2 = 0; n2 < 8; ++n2) {
+      uint32_t b[4];
+      ldsm_x4(b, &sm.k[(n2 * 16 + (lane % 8) + (lane / 16) * 8) * LD + kk * 16 + ((lane / 8) % 2) * 8]);
+      mma16816(acc[2 * n2], a, b[0], b[1]);
+      mma16816(acc[2 * n2 + 1], a, b[2], b[3]);
+    }
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void load_rows_smem(__nv_bfloat16* dst, const __nv_bfloat16* src_base, const int* rows,
+                                               int nrows, int S, bool rows_are_list, int row0) {
+  constexpr int LD = D + 8;
+  constexpr int V = D / 8;  // uint4 per row
+  for (int i = threadIdx.x; i < nrows * V; i += blockDim.x) {
+    const int r = i / V, c = i % V;
+    const int pos = rows_are_list ? rows[r] : row0 + r;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (pos >= 0 && pos < S) val = reinterpret_cast<const uint4*>(src_base + (size_t)pos * D)[c];
+    *reinterpret_cast<uint4*>(dst + r * LD + c * 8) = val;
+  }
+}
+
+// mode 0: pass 1 (row max / sum partials); mode 1: pass 2 (A-hat -> c, dg)
+template <int D>
+__global__ void __launch_bounds__(128) slab_kernel(int mode, const DSlab* __restrict__ slabs, int n_slabs,
+                                                   const __nv_bfloat16* __restrict__ q,
+                                                   const __nv_bfloat16* __restrict__ k, int S, int H,
+                                                   float scale_log2, const int* __restrict__ rows,
+                                                   const int* __restrict__ rranks, const int* __restrict__ sinfo,
+                                                   const uint8_t* __restrict__ labels, const int* __restrict__ rank,
+                                                   float2* __restrict__ ml_part, const float2* __restrict__ ml,
+                                                   float* __restrict__ cbuf, unsigned long long* __restrict__ dgbuf,
+                                                   int n_chunks) {
+  extern __shared__ __align__(16) uint8_t slab_smem_raw[];
+  SlabSmem<D>& sm = *reinterpret_cast<SlabSmem<D>*>(slab_smem_raw);
+  const int chunk = blockIdx.x, kv = blockIdx.y;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int g = lane / 4, t4 = lane % 4;
+  const int j_chunk0 = chunk * SLAB_CHUNK;
+  for (int si = 0; si < n_slabs; ++si) {
+    const DSlab sl = slabs[si];
+    if (sl.kv != kv) continue;
+    const int L = sinfo[si * 4 + 0];
+    const int maxpos = sinfo[si * 4 + 2];
+    if (L == 0 || j_chunk0 > maxpos) {
+      if (mode == 0 && threadIdx.x < SLAB_ROWS)
+        ml_part[((size_t)si * n_chunks + chunk) * SLAB_ROWS + threadIdx.x] = make_float2(-INFINITY, 0.f);
+      continue;
+    }
+    const int* srow = rows + si * SLAB_ROWS;
+    __syncthreads();
+    load_rows_smem<D>(sm.q, q + (size_t)sl.head * S * D, srow, SLAB_ROWS, S, true, 0);
+    const int r_lo = warp * 16 + g, r_hi = r_lo + 8;
+    const int pos_lo = srow[r_lo], pos_hi = srow[r_hi];
+    float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+    float mr_lo = 0.f, mr_hi = 0.f, il_lo = 0.f, il_hi = 0.f;
+    if (mode == 1) {
+      const float2 a = ml[si * SLAB_ROWS + r_lo], b = ml[si * SLAB_ROWS + r_hi];
+      mr_lo = a.x;
+      il_lo = a.y > 0.f ? 1.f / a.y : 0.f;
+      mr_hi = b.x;
+      il_hi = b.y > 0.f ? 1.f / b.y : 0.f;
+    }
+    for (int tt = 0; tt < SLAB_CHUNK / BLK; ++tt) {
+      const int j0 = j_chunk0 + tt * BLK;
+      if (j0 > maxpos) break;
+      __syncthreads();
+      load_rows_smem<D>(sm.k, k + (size_t)kv * S * D, nullptr, BLK, S, false, j0);
+      __syncthreads();
+      float acc[16][4];
+      slab_tile_scores<D>(sm, acc);
+      // mask + scale
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = j0 + nt * 8 + 2 * t4 + (e & 1);
+          const int pr = (e < 2) ? pos_lo : pos_hi;
+          acc[nt][e] = (pr >= 0 && j <= pr) ? acc[nt][e] * scale_log2 : -INFINITY;
+        }
+      }
+      if (mode == 0) {
+        float tm_lo = -INFINITY, tm_hi = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) {
+          tm_lo = fmaxf(tm_lo, fmaxf(acc[nt][0], acc[nt][1]));
+          tm_hi = fmaxf(tm_hi, fmaxf(acc[nt][2], acc[nt][3]));
+        }
+        tm_lo = fmaxf(tm_lo, __shfl_xor_sync(0xffffffffu, tm_lo, 1));
+        tm_lo = fmaxf(tm_lo, __shfl_xor_sync(0xffffffffu, tm_lo, 2));
+        tm_hi = fmaxf(tm_hi, __shfl_xor_sync(0xffffffffu, tm_hi, 1));
+        tm_hi = fmaxf(tm_hi, __shfl_xor_sync(0xffffffffu, tm_hi, 2));
+        const float nm_lo = fmaxf(m_lo, tm_lo), nm_hi = fmaxf(m_hi, tm_hi);
+        float s_lo = 0.f, s_hi = 0.f;
+        if (nm_lo > -INFINITY) {
+#pragma unroll
+          for (int nt = 0; nt < 16; ++nt) s_lo += exp2f(acc[nt][0] - nm_lo) + exp2f(acc[nt][1] - nm_lo);
+        }
+        if (nm_hi > -INFINITY) {
+#pragma unroll
+          for (int nt = 0; nt < 16; ++nt) s_hi += exp2f(acc[nt][2] - nm_hi) + exp2f(acc[nt][3] - nm_hi);
+        }
+        s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 1);
+        s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 2);
+        s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 1);
+        s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 2);
+        l_lo = (m_lo > -INFINITY ? l_lo * exp2f(m_lo - nm_lo) : 0.f) + s_lo;
+        l_hi = (m_hi > -INFINITY ? l_hi * exp2f(m_hi - nm_hi) : 0.f) + s_hi;
+        m_lo = nm_lo;
+        m_hi = nm_hi;
+      } else {
+        // A-hat tile -> smem
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) {
+          const int c = nt * 8 + 2 * t4;
+          sm.a[r_lo][c] = acc[nt][0] > -INFINITY ? exp2f(acc[nt][0] - mr_lo) * il_lo : 0.f;
+          sm.a[r_lo][c + 1] = acc[nt][1] > -INFINITY ? exp2f(acc[nt][1] - mr_lo) * il_lo : 0.f;
+          sm.a[r_hi][c] = acc[nt][2] > -INFINITY ? exp2f(acc[nt][2] - mr_hi) * il_hi : 0.f;
+          sm.a[r_hi][c + 1] = acc[nt][3] > -INFINITY ? exp2f(acc[nt][3] - mr_hi) * il_hi : 0.f;
+        }
+        if (sl.rank_mode) {
+          // compact the keys of modality qmod in this tile (ranks are consecutive)
+          const int j = j0 + threadIdx.x;
+          const bool isa = (j < S) && labels[j] == sl.qmod;
+          const unsigned bal = __ballot_sync(0xffffffffu, isa);
+          if (lane == 0) sm.red[warp] = __popc(bal);
+          __syncthreads();
+          int base = 0;
+          for (int w = 0; w < warp; ++w) base += sm.red[w];
+          if (isa) sm.colidx[base + __popc(bal & ((1u << lane) - 1u))] = threadIdx.x;
+          if (threadIdx.x == 0) sm.red[4] = sm.red[0] + sm.red[1] + sm.red[2] + sm.red[3];
+        }
+        __syncthreads();
+        // column mass: fixed order over rows
+        {
+          const int c = threadIdx.x;
+          const int j = j0 + c;
+          float sum = 0.f;
+          for (int r = 0; r < SLAB_ROWS; ++r) sum += sm.a[r][c];
+          if (j < S) cbuf[sl.c_off + j] = sum;
+        }
+        // diagonal mass -> fixed point
+        const double FX = 4503599627370496.0;  // 2^52
+        if (!sl.rank_mode) {
+          // contiguous runs of slab rows
+          int r0 = 0;
+          while (r0 < L) {
+            int r1 = r0 + 1;
+            while (r1 < L && srow[r1] == srow[r1 - 1] + 1) ++r1;
+            const int pb = srow[r0] - r0;  // pos_r = pb + r
+            const int width = 127 + (r1 - r0);
+            for (int i = threadIdx.x; i < width; i += blockDim.x) {
+              const int o = pb + r0 - (j0 + 127) + i;
+              if (o < 0) continue;
+              float sum = 0.f;
+              for (int r = r0; r < r1; ++r) {
+                const int c = pb + r - o - j0;
+                if (c >= 0 && c < BLK) sum += sm.a[r][c];
+              }
+              if (sum > 0.f) atomicAdd(dgbuf + sl.dg_off + o, (unsigned long long)((double)sum * FX));
+            }
+            r0 = r1;
+          }
+        } else {
+          const int Ka = sm.red[4];
+          if (Ka > 0) {
+            const int rank_lo = rank[j0 + sm.colidx[0]];
+            const int rho0 = rranks[si * SLAB_ROWS];  // slab ranks are consecutive
+            const int width = L + Ka - 1;
+            for (int i = threadIdx.x; i < width; i += blockDim.x) {
+              const int o = rho0 - (rank_lo + Ka - 1) + i;
+              if (o < 0) continue;
+              float sum = 0.f;
+              for (int r = 0; r < L; ++r) {
+                const int kr = rho0 + r - o - rank_lo;
+                if (kr >= 0 && kr < Ka) sum += sm.a[r][sm.colidx[kr]];
+              }
+              if (sum > 0.f) atomicAdd(dgbuf + sl.dg_off + o, (unsigned long long)((double)sum * FX));
+            }
+          }
+        }
+      }
+    }
+    if (mode == 0 && t4 == 0) {
+      ml_part[((size_t)si * n_chunks + chunk) * SLAB_ROWS + r_lo] = make_float2(m_lo, l_lo);
+      ml_part[((size_t)si * n_chunks + chunk) * SLAB_ROWS + r_hi] = make_float2(m_hi, l_hi);
+    }
+  }
+}
+
+__global__ void slab_combine_kernel(const float2* __restrict__ ml_part, int n_chunks, float2* __restrict__ ml) {
+  const int si = blockIdx.x, r = threadIdx.x;
+  float m = -INFINITY;
+  for (int c = 0; c < n_chunks; ++c) m = fmaxf(m, ml_part[((size_t)si * n_chunks + c) * SLAB_ROWS + r].x);
+  float l = 0.f;
+  if (m > -INFINITY)
+    for (int c = 0; c < n_chunks; ++c) {
+      const float2 p = ml_part[((size_t)si * n_chunks + c) * SLAB_ROWS + r];
+      if (p.x > -INFINITY) l += p.y * exp2f(p.x - m);
+    }
+  ml[si * SLAB_ROWS + r] = make_float2(m, l);
+}
+
+void launch_slabs(const DSlab* slabs, int n_slabs, const void* q, const void* k, int S, int H, int Hkv, int D,
+                  int last_q, float scale_log2, const int* info, const int* perm, const int* rank,
+                  const uint8_t* labels, int* rows, int* rranks, int* sinfo, float2* ml_part, float2* ml, float* cbuf,
+                  unsigned long long* dgbuf, int n_chunks, cudaStream_t st) {
+  if (n_slabs == 0) return;
+  slab_rows_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(slabs, S, last_q, info, perm, rank, rows, rranks, sinfo);
+  dim3 grid(n_chunks, Hkv);
+  if (D == 128) {
+    const int smem = sizeof(SlabSmem<128>);
+    cudaFuncSetAttribute(slab_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    slab_kernel<128><<<grid, 128, smem, st>>>(0, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S,
+                                              H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf,
+                                              dgbuf, n_chunks);
+    slab_combine_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(ml_part, n_chunks, ml);
+    slab_kernel<128><<<grid, 128, smem, st>>>(1, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S,
+                                              H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf,
+                                              dgbuf, n_chunks);
+  } else {
+    const int smem = sizeof(SlabSmem<64>);
+    cudaFuncSetAttribute(slab_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    slab_kernel<64><<<grid, 128, smem, st>>>(0, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S,
+                                             H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf,
+                                             dgbuf, n_chunks);
+    slab_combine_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(ml_part, n_chunks, ml);
+    slab_kernel<64><<<grid, 128, smem, st>>>(1, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S,
+                                             H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf,
+                                             dgbuf, n_chunks);
+  }
+}
+
+// =============================================================== a3: grid
+// c_rank[g][rho] = c[P_a[rho]] for rank-coordinate grid instances
+__global__ void grid_gather_rank_kernel(const DInst* __restrict__ insts, int n_inst_total, const DSlab* __restrict__ slabs,
+                                        const int* __restrict__ info, const int* __restrict__ perm,
+                                        const float* __restrict__ cbuf, float* __restrict__ c_rank, int S_pad) {
+  const int ii = blockIdx.y;
+  const DInst x = insts[ii];
+  if (x.kind != MMI_PAT_GRID || !x.rank) return;
+  const int na = info[MI_CNT + x.qa];
+  const int off = info[MI_OFF + x.qa];
+  const DSlab sl = slabs[x.slab];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < na; r += gridDim.x * blockDim.x)
+    c_rank[(size_t)x.grid_id * S_pad + r] = cbuf[sl.c_off + perm[off + r]];
+}
+
+struct JP {
+  double J;
+  int p;
+};
+__device__ __forceinline__ JP jp_best(JP a, JP b) {
+  if (b.J > a.J || (b.J == a.J && b.p < a.p)) return b;
+  return a;
+}
+
+struct JPMax {
+  __device__ __forceinline__ JP operator()(const JP& a, const JP& b) const { return jp_best(a, b); }
+};
+
+__device__ __forceinline__ void grid_window(const DInst& x, const int* sinfo, const int* info, int S, int& lo, int& hi,
+                                            int& n) {
+  n = x.rank ? info[MI_CNT + x.qa] : S;
+  const int wmin = x.rank ? sinfo[x.slab * 4 + 3] : sinfo[x.slab * 4 + 1];
+  lo = FOLD_LO;
+  hi = min(wmin - FOLD_GAP, n);
+}
+
+// T = sum_W c (fp64, fixed order)
+__global__ void grid_total_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst,
+                                  const DSlab* __restrict__ slabs, const int* __restrict__ sinfo,
+                                  const int* __restrict__ info, const float* __restrict__ cbuf,
+                                  const float* __restrict__ c_rank, int S, int S_pad, GridRes* __restrict__ res) {
+  const int gi = blockIdx.x;
+  const DInst x = insts[grid_inst[gi]];
+  int lo, hi, n;
+  grid_window(x, sinfo, info, S, lo, hi, n);
+  const float* c = x.rank ? c_rank + (size_t)gi * S_pad : cbuf + slabs[x.slab].c_off;
+  double sum = 0.0;
+  for (int j = lo + threadIdx.x; j < hi; j += blockDim.x) sum += c[j];
+  typedef cub::BlockReduce<double, 256> R;
+  __shared__ typename R::TempStorage tmp;
+  const double T = R(tmp).Sum(sum);
+  if (threadIdx.x == 0) {
+    res[gi].T = T;
+    res[gi].valid = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) grid_fold_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst,
+                                                        const DSlab* __restrict__ slabs, const int* __restrict__ sinfo,
+                                                        const int* __restrict__ info, const float* __restrict__ cbuf,
+                                                        const float* __restrict__ c_rank, int S, int S_pad,
+                                                        const GridRes* __restrict__ res, double* __restrict__ part) {
+  const int gi = blockIdx.y;
+  const DInst x = insts[grid_inst[gi]];
+  const int s = x.smin + blockIdx.x;
+  double* out = part + ((size_t)gi * 1025 + blockIdx.x) * 2;
+  if (s > x.smax) return;
+  int lo, hi, n;
+  grid_window(x, sinfo, info, S, lo, hi, n);
+  const int N = hi - lo;
+  if (N < s || s < 1) {
+    if (threadIdx.x == 0) {
+      out[0] = -INFINITY;
+      out[1] = 0;
+    }
+    return;
+  }
+  const float* c = x.rank ? c_rank + (size_t)gi * S_pad : cbuf + slabs[x.slab].c_off;
+  const double T = res[gi].T;
+  __shared__ double part_s[256];
+  typedef cub::BlockReduce<JP, 256> R;
+  __shared__ typename R::TempStorage tmp;
+  JP best;
+  best.J = -INFINITY;
+  best.p = INT_MAX;
+  if (s <= 256) {
+    const int G = 256 / s;
+    const int tid = threadIdx.x;
+    double acc = 0.0;
+    if (tid < G * s) {
+      const int grp = tid / s, p = tid % s;
+      const int j0 = lo + (((p - lo) % s) + s) % s;
+      for (int j = j0 + grp * s; j < hi; j += G * s) acc += c[j];
+    }
+    part_s[tid] = acc;
+    __syncthreads();
+    if (tid < s) {
+      double m = 0.0;
+      for (int grp = 0; grp < G; ++grp) m += part_s[grp * s + tid];
+      const int p = tid;
+      const int j0 = lo + (((p - lo) % s) + s) % s;
+      const int np = j0 < hi ? (hi - 1 - j0) / s + 1 : 0;
+      best.J = m - (double)np * T / (double)N;
+      best.p = p;
+    }
+  } else {
+    for (int p = threadIdx.x; p < s; p += 256) {
+      const int j0 = lo + (((p - lo) % s) + s) % s;
+      double m = 0.0;
+      for (int j = j0; j < hi; j += s) m += c[j];
+      const int np = j0 < hi ? (hi - 1 - j0) / s + 1 : 0;
+      JP cand;
+      cand.J = m - (double)np * T / (double)N;
+      cand.p = p;
+      best = jp_best(best, cand);
+    }
+  }
+  const JP b = R(tmp).Reduce(best, JPMax());
+  if (threadIdx.x == 0) {
+    out[0] = b.J;
+    out[1] = (double)b.p;
+  }
+}
+
+__global__ void grid_pick_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst, int n_grid,
+                                 const double* __restrict__ part, GridRes* __restrict__ res) {
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= n_grid) return;
+  const DInst x = insts[grid_inst[gi]];
+  double bJ = -INFINITY;
+  int bs = x.smin, bp = 0, valid = 0;
+  for (int s = x.smin; s <= x.smax; ++s) {
+    const double J = part[((size_t)gi * 1025 + (s - x.smin)) * 2];
+    if (J == -INFINITY) continue;
+    if (!valid || J > bJ) {
+      bJ = J;
+      bs = s;
+      bp = (int)part[((size_t)gi * 1025 + (s - x.smin)) * 2 + 1];
+      valid = 1;
+    }
+  }
+  res[gi].s = bs;
+  res[gi].p = valid ? bp : 0;
+  res[gi].J = valid ? bJ : 0.0;
+  res[gi].valid = valid;
+}
+
+void launch_grid(const DInst* insts, const int* grid_inst, int n_grid, int max_ncand, int n_inst_total,
+                 const DSlab* slabs, const int* sinfo, const int* info, const int* perm, const float* cbuf,
+                 float* c_rank, int S, int S_pad, GridRes* res, double* part, cudaStream_t st) {
+  if (n_grid == 0) return;
+  grid_gather_rank_kernel<<<dim3(64, n_inst_total), 256, 0, st>>>(insts, n_inst_total, slabs, info, perm, cbuf,
+                                                                   c_rank, S_pad);
+  grid_total_kernel<<<n_grid, 256, 0, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S, S_pad, res);
+  grid_fold_kernel<<<dim3(max_ncand, n_grid), 256, 0, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S,
+                                                            S_pad, res, part);
+  grid_pick_kernel<<<(n_grid + 63) / 64, 64, 0, st>>>(insts, grid_inst, n_grid, part, res);
+}
+
+// =============================================================== a4: VS top-k
+// Candidates i in [0, n_cand); key(i) = float bits of the score (>= 0).  Selects
+// the top `need` by (score desc, index asc) and writes their coordinates in
+// ascending order after an optional forced 0.
+struct VSCtx {
+  int mode;        // 0: columns POS, 1: columns RANK (modality a), 2: columns cross (modality b), 3: offsets
+  const float* c;
+  const unsigned long long* dg;
+  const int* perm;
+  int off;         // perm offset of the modality
+};
+__device__ __forceinline__ uint32_t vs_key(const VSCtx& x, int i) {
+  float v;
+  if (x.mode == 0)
+    v = x.c[i];
+  else if (x.mode == 1 || x.mode == 2)
+    v = x.c[x.perm[x.off + i]];
+  else
+    v = (float)((double)x.dg[i] * (1.0 / 4503599627370496.0));
+  return __float_as_uint(fmaxf(v, 0.f));
+}
+
+__global__ void __launch_bounds__(1024) vs_select_kernel(const DInst* __restrict__ insts, const int* __restrict__ vs_inst,
+                                                         const DSlab* __restrict__ slabs, const int* __restrict__ sinfo,
+                                                         const int* __restrict__ info, const int* __restrict__ perm,
+                                                         const float* __restrict__ cbuf,
+                                                         const unsigned long long* __restrict__ dgbuf,
+                                                         const int64_t* __restrict__ list_off,
+                                                         const int64_t* __restrict__ bits_off, int* __restrict__ lists,
+                                                         int* __restrict__ counts, uint32_t* __restrict__ bits) {
+  const int vi = blockIdx.x, which = blockIdx.y;  // which 0: verticals, 1: slashes
+  const DInst x = insts[vs_inst[vi]];
+  const DSlab sl = slabs[x.slab];
+  const bool cross = (x.kb >= 0 && x.kb != x.qa);
+  const int n_req = which == 0 ? x.n_v : x.n_s;
+  int* out = lists + list_off[vi * 2 + which];
+  uint32_t* obits = bits + bits_off[vi * 2 + which];
+  if (which == 1 && (cross || n_req <= 0)) {
+    if (threadIdx.x == 0) counts[vi * 2 + 1] = 0;
+    return;
+  }
+  VSCtx ctx;
+  ctx.c = cbuf + sl.c_off;
+  ctx.dg = dgbuf + sl.dg_off;
+  ctx.perm = perm;
+  ctx.off = 0;
+  int n_cand;
+  const int maxpos = sinfo[x.slab * 4 + 2];
+  const int L = sinfo[x.slab * 4 + 0];
+  const int maxrank = sinfo[x.slab * 4 + 3] + L - 1;
+  if (which == 0) {
+    if (cross) {
+      ctx.mode = 2;
+      ctx.off = info[MI_OFF + x.kb];
+      // number of keys of modality kb with position <= maxpos
+      const int nb_ = info[MI_CNT + x.kb];
+      int lo = 0, hi = nb_;
+      while (lo < hi) {
+        const int mid = (lo + hi) / 2;
+        if (perm[ctx.off + mid] <= maxpos)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      n_cand = lo;
+    } else if (x.rank) {
+      ctx.mode = 1;
+      ctx.off = info[MI_OFF + x.qa];
+      n_cand = maxrank + 1;
+    } else {
+      ctx.mode = 0;
+      n_cand = maxpos + 1;
+    }
+  } else {
+    ctx.mode = 3;
+    n_cand = (x.rank ? maxrank : maxpos) + 1;
+  }
+  const int force = x.force ? 1 : 0;
+  const int lo_i = force;  // candidate indices [lo_i, n_cand)
+  const int N = max(0, n_cand - lo_i);
+  const int need = min(max(n_req - force, 0), N);
+
+  __shared__ int hist[256];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_k;
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage stmp;
+  __shared__ int s_carry_eq, s_carry_out;
+
+  uint32_t prefix = 0, pmask = 0;
+  int k = need;  // rank (1-based) of the threshold among remaining
+  const bool take_all = (need >= N);
+  if (!take_all && need > 0) {
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int i = lo_i + threadIdx.x; i < n_cand; i += blockDim.x) {
+        const uint32_t key = vs_key(ctx, i);
+        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int kk = k, b = 255;
+        for (; b >= 0; --b) {
+          if (hist[b] >= kk) break;
+          kk -= hist[b];
+        }
+        s_prefix = prefix | ((uint32_t)b << shift);
+        s_k = kk;
+      }
+      __syncthreads();
+      prefix = s_prefix;
+      k = s_k;
+      pmask |= 255u << shift;
+      __syncthreads();
+    }
+  }
+  const uint32_t T = prefix;  // threshold key; take all > T and the first k == T (index order)
+  if (threadIdx.x == 0) {
+    s_carry_eq = 0;
+    s_carry_out = force;
+    if (force) out[0] = 0;
+  }
+  __syncthreads();
+  if (need > 0) {
+    for (int base = lo_i; base < n_cand; base += blockDim.x) {
+      const int i = base + threadIdx.x;
+      int gt = 0, eq = 0;
+      if (i < n_cand) {
+        if (take_all) {
+          gt = 1;
+        } else {
+          const uint32_t key = vs_key(ctx, i);
+          gt = key > T;
+          eq = key == T;
+        }
+      }
+      int eq_pre;
+      Scan(stmp).ExclusiveSum(eq, eq_pre);
+      __syncthreads();
+      const int sel = gt || (eq && (s_carry_eq + eq_pre) < k);
+      int sel_pre, sel_tot;
+      Scan(stmp).ExclusiveSum(sel, sel_pre, sel_tot);
+      __syncthreads();
+      int eq_tot = 0;
+      if (threadIdx.x == blockDim.x - 1) eq_tot = eq_pre + eq;
+      if (sel) {
+        const int coord = (ctx.mode == 2) ? perm[ctx.off + i] : i;
+        out[s_carry_out + sel_pre] = coord;
+      }
+      __syncthreads();
+      if (threadIdx.x == blockDim.x - 1) {
+        s_carry_eq += eq_tot;
+        s_carry_out += sel_tot;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  const int total = s_carry_out;
+  if (threadIdx.x == 0) counts[vi * 2 + which] = total;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int cdn = out[i];
+    atomicOr(obits + (cdn >> 5), 1u << (cdn & 31));
+  }
+}
+
+void launch_vs(const DInst* insts, const int* vs_inst, int n_vs, const DSlab* slabs, const int* sinfo, const int* info,
+               const int* perm, const float* cbuf, const unsigned long long* dgbuf, const int64_t* list_off,
+               const int64_t* bits_off, int* lists, int* counts, uint32_t* bits, cudaStream_t st) {
+  if (n_vs == 0) return;
+  vs_select_kernel<<<dim3(n_vs, 2), 1024, 0, st>>>(insts, vs_inst, slabs, sinfo, info, perm, cbuf, dgbuf, list_off,
+                                                    bits_off, lists, counts, bits);
+}
+
+}  // namespace mmi

@@ -1,0 +1,756 @@
+// Index construction, permutation gathers (a6) and the
+// inverse-permute LSE merge (a8).
+//
+// Views are position lists in the gathered Q̄ / K̄ spaces (Alg.1 P:213 row- and
+// column-wise grid permutation, Alg.2/3 P:254/P:340 modality permutation,
+// P:708 "convert them into a sparse format i_vs").  Work items are 128-row
+// blocks of a Q-view with a list of segments (runs of key tiles of a K-view)
+// and an element role; their union per row is exactly the paper's mask, each
+// admitted element owned by exactly one pass (reading C9).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <climits>
+#include <cstdint>
+
+#include "estimate.h"
+#include "index.h"
+
+namespace mmi {
+
+__device__ __forceinline__ int pad128d(int x) { return (x + BLK - 1) / BLK * BLK; }
+__device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// class geometry of an arithmetic residue view over base coords [0, n)
+struct ClassGeo {
+  int n, s, q, rem, padq1, padq;
+  __device__ __forceinline__ void init(int n_, int s_) {
+    n = n_;
+    s = s_;
+    q = n / s;
+    rem = n % s;
+    padq1 = pad128d(q + 1);
+    padq = pad128d(q);
+  }
+  __device__ __forceinline__ int nr(int r) const { return q + (r < rem ? 1 : 0); }
+  __device__ __forceinline__ int classoff(int r) const {
+    return min(r, rem) * padq1 + max(0, r - rem) * padq;
+  }
+  __device__ __forceinline__ int total() const { return rem * padq1 + (s - rem) * padq; }
+  // RES view row -> (r, t); false if beyond the view
+  __device__ __forceinline__ bool locate(int row, int& r, int& t) const {
+    const int a = rem * padq1;
+    if (row < a) {
+      r = row / padq1;
+      t = row % padq1;
+      return true;
+    }
+    if (padq == 0) return false;
+    const int b = row - a;
+    r = rem + b / padq;
+    t = b % padq;
+    return r < s;
+  }
+};
+
+__device__ __forceinline__ int lower_bound_i(const int* a, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int upper_bound_i(const int* a, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// ================================================================ views
+__global__ void build_views_kernel(IndexCtx C, int space, const int* __restrict__ view_ids, int n_view_ids,
+                                   int64_t rows_total) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows_total) return;
+  // find the view containing this row
+  int lo = 0, hi = n_view_ids - 1, v = -1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const DView& dv = C.views[view_ids[mid]];
+    if (row < dv.row_off)
+      hi = mid - 1;
+    else if (row >= (int64_t)dv.row_off + dv.cap)
+      lo = mid + 1;
+    else {
+      v = view_ids[mid];
+      break;
+    }
+  }
+  int* pos_a = space ? C.kg_pos : C.qg_pos;
+  int* rank_a = space ? C.kg_rank : C.qg_rank;
+  int* src_a = space ? C.kg_src : C.qg_src;
+  const int PADPOS = space ? KPAD : -1;
+  if (v < 0) {
+    pos_a[row] = PADPOS;
+    rank_a[row] = PADPOS;
+    src_a[row] = -2;
+    return;
+  }
+  const DView dv = C.views[v];
+  const int i = (int)(row - dv.row_off);
+  const int h = dv.head;
+  const int srcbase = space ? (C.heads[h].kv * C.S) : (h * C.S);
+  int pos = -1, rk = -1, len = 0;
+  bool valid = false;
+  if (dv.kind == VK_MOD) {
+    len = C.info[MI_PADOFF + MAX_MOD];
+    if (i < len) {
+      pos = C.modpos[i];
+      valid = pos >= 0;
+      if (valid) rk = C.rank[pos];
+    }
+  } else if (dv.kind == VK_ORIG_CLASS || dv.kind == VK_RANK_CLASS) {
+    const DInst x = C.insts[h * MAX_INST + dv.inst];
+    const GridRes g = C.gridres[x.grid_id];
+    const bool rnk = dv.kind == VK_RANK_CLASS;
+    const int n = rnk ? C.info[MI_CNT + dv.mod] : C.S;
+    int coord = -1;
+    if (dv.classes == 1) {
+      const int np = g.p < n ? (n - g.p + g.s - 1) / g.s : 0;
+      len = pad128d(np);
+      if (i < np) coord = g.p + g.s * i;
+    } else {
+      ClassGeo cg;
+      cg.init(n, g.s);
+      len = cg.total();
+      int r, t;
+      if (i < len && cg.locate(i, r, t) && t < cg.nr(r)) coord = r + g.s * t;
+    }
+    if (coord >= 0) {
+      valid = true;
+      if (rnk) {
+        pos = C.perm[C.info[MI_OFF + dv.mod] + coord];
+        rk = coord;
+      } else {
+        pos = coord;
+        rk = C.rank[pos];
+      }
+    }
+  } else if (dv.kind == VK_VCOL) {
+    const DInst x = C.insts[h * MAX_INST + dv.inst];
+    const int cnt = C.vs_cnt[x.vs_id * 2];
+    len = pad128d(cnt);
+    if (i < cnt) {
+      const int coord = C.vs_lists[C.vs_list_off[x.vs_id * 2] + i];
+      valid = true;
+      if (x.rank) {
+        pos = C.perm[C.info[MI_OFF + x.qa] + coord];
+        rk = coord;
+      } else {
+        pos = coord;
+        rk = C.rank[pos];
+      }
+    }
+  }
+  if (i == 0) C.view_len[v] = len;
+  if (valid) {
+    pos_a[row] = pos;
+    rank_a[row] = rk;
+    src_a[row] = srcbase + pos;
+  } else {
+    pos_a[row] = PADPOS;
+    rank_a[row] = PADPOS;
+    src_a[row] = (i < len) ? -1 : -2;
+  }
+}
+
+// ================================================================ instance params
+__global__ void inst_params_kernel(IndexCtx C, int n_total) {
+  const int ii = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ii >= n_total) return;
+  const DInst x = C.insts[ii];
+  InstParam ip;
+  ip.sink = x.sink;
+  ip.local = x.local;
+  ip.s = ip.p = 0;
+  ip.slash_word = ip.vmask_word = -1;
+  ip.pad0 = ip.pad1 = 0;
+  if (x.kind == MMI_PAT_GRID) {
+    const GridRes g = C.gridres[x.grid_id];
+    ip.s = g.s;
+    ip.p = g.p;
+  }
+  if (x.kind == MMI_PAT_VSLASH) {
+    ip.vmask_word = (int)C.vs_bits_off[x.vs_id * 2];
+    ip.slash_word = (int)C.vs_bits_off[x.vs_id * 2 + 1];
+  }
+  C.inst_params[ii] = ip;
+}
+
+// ================================================================ items / segments
+struct RowsInfo {
+  int xp_lo, xp_hi;   // positions of first / last valid row
+  int xr_lo, xr_hi;   // modality ranks (rank-coordinate views)
+};
+
+struct Emitter {
+  Seg* out;        // nullptr => count only
+  int n_segs, n_tiles;
+  __device__ __forceinline__ void add(int krow0, int ntiles, uint32_t meta, int ph, int pt) {
+    if (ntiles <= 0) return;
+    if (out) {
+      Seg s;
+      s.krow0 = krow0;
+      s.ntiles = ntiles;
+      s.meta = meta;
+      s.pred_head = (int16_t)min(ph, 32767);
+      s.pred_tail = (int16_t)min(pt, 32767);
+      out[n_segs] = s;
+    }
+    ++n_segs;
+    n_tiles += ntiles;
+  }
+};
+
+// A K-view for emission: maps tile t -> coords / positions, krow.
+struct KView {
+  int kind;          // 0 ORIG K, 1 MOD region (rank coords), 2 class view (CLS / one RES class), 3 VCOL
+  int space;
+  int row0;          // K-space row of tile 0
+  int n;             // valid keys
+  int kv_base;       // ORIG: kv*S
+  // class views
+  int cls_r, cls_s;
+  const int* pos_of_rank;  // MOD / rank-class: P_b (positions by rank), else nullptr
+  const int* list;         // VCOL coords
+  int list_rank;           // VCOL coords are ranks (use pos_of_rank)
+  __device__ __forceinline__ int coord_at(int i) const {
+    if (kind == 0) return i;
+    if (kind == 1) return i;
+    if (kind == 2) return cls_r + cls_s * i;
+    return list[i];
+  }
+  __device__ __forceinline__ int pos_at(int i) const {
+    const int c = coord_at(i);
+    if (kind == 0) return c;
+    if (kind == 1) return pos_of_rank[c];
+    if (kind == 2) return pos_of_rank ? pos_of_rank[c] : c;
+    return list_rank ? pos_of_rank[c] : c;
+  }
+};
+
+__device__ __forceinline__ bool tile_full(const KView& kv, int t, uint32_t role, int rmode, const RowsInfo& R,
+                                          int sink, int local) {
+  const int i0 = t * BLK, i1 = min(t * BLK + BLK - 1, kv.n - 1);
+  if (t * BLK + BLK - 1 >= kv.n) return false;  // pads present
+  const int yp_hi = kv.pos_at(i1);
+  if (yp_hi > R.xp_lo) return false;            // not causally full
+  if (role == R_TRUE) return true;
+  if (role == R_VSSL) return false;
+  const int y_lo = rmode ? (kv.kind == 0 ? i0 : kv.coord_at(i0)) : kv.pos_at(i0);
+  const int y_hi = rmode ? (kv.kind == 0 ? i1 : kv.coord_at(i1)) : yp_hi;
+  const int x_lo = rmode ? R.xr_lo : R.xp_lo;
+  const int x_hi = rmode ? R.xr_hi : R.xp_hi;
+  if (role == R_A) return (y_hi < sink) || (x_hi - y_lo < local);
+  // R_NOTA
+  return (y_lo >= sink) && (x_lo - y_hi >= local);
+}
+
+// emit tiles [t0, t1) of a K-view, split into segments of the form PRED* FULL* PRED*
+__device__ void emit_range(Emitter& E, const KView& kv, int t0, int t1, uint32_t role, int rmode, uint32_t inst,
+                           const RowsInfo& R, int sink, int local) {
+  const uint32_t meta = seg_meta(kv.space, role, rmode, inst);
+  int t = t0;
+  while (t < t1) {
+    const int start = t;
+    int ph = 0, nfull = 0, pt = 0;
+    while (t < t1 && !tile_full(kv, t, role, rmode, R, sink, local)) {
+      ++ph;
+      ++t;
+    }
+    while (t < t1 && tile_full(kv, t, role, rmode, R, sink, local)) {
+      ++nfull;
+      ++t;
+    }
+    while (t < t1 && !tile_full(kv, t, role, rmode, R, sink, local)) {
+      ++pt;
+      ++t;
+    }
+    E.add(kv.row0 + start * BLK, t - start, meta, ph, pt);
+  }
+}
+
+// tiles of a K-view whose key coordinate range intersects [c_lo, c_hi] (coords ascending)
+__device__ __forceinline__ void coord_tiles(const KView& kv, int c_lo, int c_hi, int& t0, int& t1) {
+  if (c_hi < c_lo || kv.n == 0) {
+    t0 = t1 = 0;
+    return;
+  }
+  int i_lo, i_hi;
+  if (kv.kind == 0 || kv.kind == 1) {
+    i_lo = max(c_lo, 0);
+    i_hi = min(c_hi, kv.n - 1);
+  } else if (kv.kind == 2) {
+    i_lo = c_lo <= kv.cls_r ? 0 : cdiv(c_lo - kv.cls_r, kv.cls_s);
+    i_hi = c_hi < kv.cls_r ? -1 : min((c_hi - kv.cls_r) / kv.cls_s, kv.n - 1);
+  } else {
+    i_lo = lower_bound_i(kv.list, kv.n, c_lo);
+    i_hi = upper_bound_i(kv.list, kv.n, c_hi) - 1;
+  }
+  if (i_hi < i_lo) {
+    t0 = t1 = 0;
+    return;
+  }
+  t0 = i_lo / BLK;
+  t1 = i_hi / BLK + 1;
+}
+
+// MOD region of modality b in POS coordinates (cross pairs): keys with position in [p_lo, p_hi]
+__device__ __forceinline__ void pos_tiles_mod(const int* Pb, int nb_, int p_lo, int p_hi, int& t0, int& t1) {
+  const int i_lo = lower_bound_i(Pb, nb_, p_lo);
+  const int i_hi = upper_bound_i(Pb, nb_, p_hi) - 1;
+  if (i_hi < i_lo) {
+    t0 = t1 = 0;
+    return;
+  }
+  t0 = i_lo / BLK;
+  t1 = i_hi / BLK + 1;
+}
+
+struct ItemCtx {
+  int h, kv;
+  const DHead* hd;
+};
+
+// K-view of the pattern's key base (No/Q: original K; 2D: modality region kb)
+__device__ KView base_kview(const IndexCtx& C, const ItemCtx& I, const DInst& x) {
+  KView k;
+  k.cls_r = 0;
+  k.cls_s = 1;
+  k.list = nullptr;
+  k.list_rank = 0;
+  if (I.hd->boundary == MMI_BND_2D) {
+    const int b = x.kb;
+    k.kind = 1;
+    k.space = 1;
+    k.row0 = C.views[I.hd->kmod_view].row_off + C.info[MI_PADOFF + b];
+    k.n = C.info[MI_CNT + b];
+    k.kv_base = 0;
+    k.pos_of_rank = C.perm + C.info[MI_OFF + b];
+  } else {
+    k.kind = 0;
+    k.space = 0;
+    k.row0 = I.kv * C.S;
+    k.n = C.S;
+    k.kv_base = I.kv * C.S;
+    k.pos_of_rank = nullptr;
+  }
+  return k;
+}
+
+// segments of one pattern instance for MAIN-type rows (and 2D cross pairs of HROW rows)
+__device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& E, const RowsInfo& R) {
+  const DInst x = C.insts[I.h * MAX_INST + ii];
+  if (x.kind == MMI_PAT_NONE) return;
+  KView kb = base_kview(C, I, x);
+  const int rmode = x.rank;
+  const bool cross_pos = (I.hd->boundary == MMI_BND_2D) && !x.rank;  // keys of modality kb, POS coords
+  const int x_lo = rmode ? R.xr_lo : R.xp_lo;
+  const int x_hi = rmode ? R.xr_hi : R.xp_hi;
+  auto range_coords = [&](int c_lo, int c_hi, int& t0, int& t1) {
+    if (cross_pos)
+      pos_tiles_mod(kb.pos_of_rank, kb.n, c_lo, c_hi, t0, t1);
+    else
+      coord_tiles(kb, c_lo, c_hi, t0, t1);
+  };
+  if (x.kind == MMI_PAT_FULL) {
+    int t0, t1;
+    range_coords(0, x_hi, t0, t1);
+    emit_range(E, kb, 0, t1, R_TRUE, rmode, ii, R, 0, 0);
+    return;
+  }
+  if (x.kind == MMI_PAT_ASHAPE || x.kind == MMI_PAT_GRID) {
+    int a0, a1, b0, b1;
+    range_coords(0, min(x.sink - 1, x_hi), a0, a1);
+    range_coords(max(0, x_lo - x.local + 1), x_hi, b0, b1);
+    if (a1 > a0 && b1 > b0 && b0 <= a1) {  // overlapping / adjacent -> one range
+      emit_range(E, kb, min(a0, b0), max(a1, b1), R_A, rmode, ii, R, x.sink, x.local);
+    } else {
+      if (a1 > a0) emit_range(E, kb, a0, a1, R_A, rmode, ii, R, x.sink, x.local);
+      if (b1 > b0) emit_range(E, kb, b0, b1, R_A, rmode, ii, R, x.sink, x.local);
+    }
+    if (x.kind == MMI_PAT_GRID && (x.flags & GF_V)) {
+      const GridRes g = C.gridres[x.grid_id];
+      const DView cv = C.views[x.v_cls_k];
+      KView kc;
+      kc.kind = 2;
+      kc.space = 1;
+      kc.row0 = cv.row_off;
+      const int n = rmode ? C.info[MI_CNT + x.qa] : C.S;
+      kc.n = g.p < n ? (n - g.p + g.s - 1) / g.s : 0;
+      kc.cls_r = g.p;
+      kc.cls_s = g.s;
+      kc.pos_of_rank = rmode ? C.perm + C.info[MI_OFF + x.qa] : nullptr;
+      kc.list = nullptr;
+      kc.list_rank = 0;
+      int t0, t1;
+      coord_tiles(kc, 0, x_hi, t0, t1);
+      emit_range(E, kc, 0, t1, R_NOTA, rmode, ii, R, x.sink, x.local);
+    }
+    return;
+  }
+  if (x.kind == MMI_PAT_VSLASH) {
+    const DView vv = C.views[x.v_vcol];
+    KView kc;
+    kc.kind = 3;
+    kc.space = 1;
+    kc.row0 = vv.row_off;
+    kc.n = C.vs_cnt[x.vs_id * 2];
+    kc.cls_r = 0;
+    kc.cls_s = 1;
+    kc.list = C.vs_lists + C.vs_list_off[x.vs_id * 2];
+    kc.list_rank = rmode;
+    kc.pos_of_rank = rmode ? C.perm + C.info[MI_OFF + x.qa] : nullptr;
+    {
+      // vertical columns: coords of the list (positions, or ranks in rank mode) <= x_hi
+      int t0, t1;
+      coord_tiles(kc, 0, cross_pos ? R.xp_hi : x_hi, t0, t1);
+      emit_range(E, kc, 0, t1, R_TRUE, rmode, ii, R, 0, 0);
+    }
+    if (!cross_pos) {
+      // slash offsets: key coords [x_lo - o, x_hi - o]; ranges move left as o grows
+      const int ns = C.vs_cnt[x.vs_id * 2 + 1];
+      const int* sl = C.vs_lists + C.vs_list_off[x.vs_id * 2 + 1];
+      int cl = 0, ch = -1;
+      const uint32_t meta = seg_meta(kb.space, R_VSSL, rmode, ii);
+      for (int q = 0; q < ns; ++q) {
+        const int o = sl[q];
+        const int c_hi = x_hi - o;
+        if (c_hi < 0) break;
+        const int c_lo = max(0, x_lo - o);
+        int t0, t1;
+        coord_tiles(kb, c_lo, c_hi, t0, t1);
+        if (t1 <= t0) continue;
+        if (ch < cl) {
+          cl = t0;
+          ch = t1 - 1;
+        } else if (t1 - 1 >= cl - 1) {
+          cl = min(cl, t0);
+        } else {
+          E.add(kb.row0 + cl * BLK, ch - cl + 1, meta, ch - cl + 1, 0);
+          cl = t0;
+          ch = t1 - 1;
+        }
+      }
+      if (ch >= cl) E.add(kb.row0 + cl * BLK, ch - cl + 1, meta, ch - cl + 1, 0);
+    }
+    return;
+  }
+}
+
+// builds (or counts) one work-item slot
+__device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W) {
+  // locate the pass
+  int lo = 0, hi = C.n_passes - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (C.passes[mid].slot_base <= slot)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const DPass ps = C.passes[lo];
+  const int b = slot - ps.slot_base;
+  ItemCtx I;
+  I.h = ps.head;
+  I.hd = &C.heads[ps.head];
+  I.kv = I.hd->kv;
+  const DHead& hd = *I.hd;
+  W.head = I.h;
+  W.q_row0 = 0;
+  W.seg_off = 0;
+  W.n_segs = 0;
+  W.n_tiles = 0;
+  W.q_gathered = 0;
+  W.out_mode = OUT_FINAL;
+  W.out_row0 = 0;
+  W.inst_base = I.h * MAX_INST;
+  W.skip_s = W.skip_p = W.skip_rank = 0;
+  W.row_mod = -1;
+  W.pad[0] = W.pad[1] = W.pad[2] = 0;
+  RowsInfo R;
+  if (ps.pass == PASS_MAIN) {
+    int grp;
+    if (hd.qmod_view < 0) {
+      const int p0 = b * BLK;
+      if (p0 >= C.S) return;
+      R.xp_lo = p0;
+      R.xp_hi = min(C.S, p0 + BLK) - 1;
+      R.xr_lo = R.xr_hi = 0;
+      W.q_row0 = I.h * C.S + p0;
+      grp = 0;
+    } else {
+      const int i0 = b * BLK;
+      if (i0 >= C.info[MI_PADOFF + MAX_MOD]) return;
+      const int p0 = C.modpos[i0];
+      if (p0 < 0) return;
+      const int a = C.labels[p0];
+      const int ilast = min(i0 + BLK - 1, C.info[MI_PADOFF + a] + C.info[MI_CNT + a] - 1);
+      R.xp_lo = p0;
+      R.xp_hi = C.modpos[ilast];
+      R.xr_lo = C.rank[p0];
+      R.xr_hi = C.rank[R.xp_hi];
+      W.q_row0 = C.views[hd.qmod_view].row_off + i0;
+      W.q_gathered = 1;
+      grp = a;
+    }
+    // skip rows owned by the HROW pass; partial output when the group has a slash pass
+    for (int ii = 0; ii < hd.n_inst; ++ii) {
+      const DInst x = C.insts[I.h * MAX_INST + ii];
+      const bool mine = (x.qa < 0) || (x.qa == grp && (x.kb < 0 || x.kb == grp));
+      if (!mine || x.kind != MMI_PAT_GRID) continue;
+      const GridRes g = C.gridres[x.grid_id];
+      if (x.flags & GF_H) {
+        W.skip_s = g.s;
+        W.skip_p = g.p;
+        W.skip_rank = x.rank;
+      }
+    }
+    if (hd.sl_inst[grp] >= 0) {
+      W.out_mode = OUT_PARTIAL;
+      W.out_row0 = hd.part_rows0 + b * BLK;
+    }
+    for (int ii = 0; ii < hd.n_inst; ++ii) {
+      const DInst x = C.insts[I.h * MAX_INST + ii];
+      if (x.qa >= 0 && x.qa != grp) continue;
+      emit_main(C, I, ii, E, R);
+    }
+  } else {
+    const int ii = ps.inst;
+    const DInst x = C.insts[I.h * MAX_INST + ii];
+    const GridRes g = C.gridres[x.grid_id];
+    const int n = x.rank ? C.info[MI_CNT + x.qa] : C.S;
+    const int* P_a = x.rank ? C.perm + C.info[MI_OFF + x.qa] : nullptr;
+    int r, t0;
+    if (ps.pass == PASS_HROW) {
+      r = g.p;
+      t0 = b * BLK;
+      const DView qv = C.views[x.v_cls_q];
+      W.q_row0 = qv.row_off + t0;
+    } else {
+      ClassGeo cg;
+      cg.init(n, g.s);
+      if (!cg.locate(b * BLK, r, t0)) return;
+      if (b * BLK >= cg.total()) return;
+      if (r == g.p && (x.flags & (GF_H | GF_V))) return;  // class p owned by H / V passes (C9)
+      const DView qv = C.views[x.v_res_q];
+      W.q_row0 = qv.row_off + b * BLK;
+      W.out_mode = OUT_PARTIAL;
+      W.out_row0 = x.pad[0] + b * BLK;
+    }
+    const int nr = r < n ? (n - r + g.s - 1) / g.s : 0;
+    if (t0 >= nr) return;
+    const int tl = min(t0 + BLK - 1, nr - 1);
+    const int c_lo = r + g.s * t0, c_hi = r + g.s * tl;
+    W.q_gathered = 1;
+    W.row_mod = ps.qa;
+    if (x.rank) {
+      R.xr_lo = c_lo;
+      R.xr_hi = c_hi;
+      R.xp_lo = P_a[c_lo];
+      R.xp_hi = P_a[c_hi];
+    } else {
+      R.xp_lo = c_lo;
+      R.xp_hi = c_hi;
+      R.xr_lo = R.xr_hi = 0;
+    }
+    if (ps.pass == PASS_HROW) {
+      // the whole causal row of the pattern's key base (role TRUE)
+      DInst xf = x;
+      xf.kind = MMI_PAT_FULL;
+      KView kb = base_kview(C, I, xf);
+      int tt0, tt1;
+      coord_tiles(kb, 0, x.rank ? R.xr_hi : R.xp_hi, tt0, tt1);
+      emit_range(E, kb, 0, tt1, R_TRUE, x.rank, ii, R, 0, 0);
+      if (hd.boundary == MMI_BND_2D) {
+        for (int jj = 0; jj < hd.n_inst; ++jj) {
+          const DInst y = C.insts[I.h * MAX_INST + jj];
+          if (y.qa == x.qa && y.kb != x.qa) emit_main(C, I, jj, E, R);
+        }
+      }
+    } else {
+      // same residue class of the key base, causal, minus the A-part (role NOTA)
+      const DView kvw = C.views[x.v_res_k];
+      ClassGeo cg;
+      cg.init(n, g.s);
+      KView kc;
+      kc.kind = 2;
+      kc.space = 1;
+      kc.row0 = kvw.row_off + cg.classoff(r);
+      kc.n = nr;
+      kc.cls_r = r;
+      kc.cls_s = g.s;
+      kc.pos_of_rank = P_a;
+      kc.list = nullptr;
+      kc.list_rank = 0;
+      int tt0, tt1;
+      coord_tiles(kc, 0, c_hi, tt0, tt1);
+      emit_range(E, kc, 0, tt1, R_NOTA, x.rank, ii, R, x.sink, x.local);
+    }
+  }
+}
+
+__global__ void items_count_kernel(IndexCtx C) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= C.n_slots) return;
+  Emitter E;
+  E.out = nullptr;
+  E.n_segs = E.n_tiles = 0;
+  WorkItem W;
+  build_slot(C, slot, E, W);
+  C.seg_cnt[slot] = E.n_segs;
+}
+
+__global__ void items_fill_kernel(IndexCtx C) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= C.n_slots) return;
+  Emitter E;
+  const int off = C.seg_off[slot];
+  E.out = C.segs + off;
+  E.n_segs = E.n_tiles = 0;
+  WorkItem W;
+  build_slot(C, slot, E, W);
+  W.seg_off = off;
+  W.n_segs = E.n_segs;
+  W.n_tiles = E.n_tiles;
+  C.items[slot] = W;
+  C.sort_keys[slot] = E.n_tiles;
+  C.sort_vals[slot] = slot;
+}
+
+__global__ void items_gather_kernel(IndexCtx C) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= C.n_slots) return;
+  C.items_sorted[i] = C.items[C.sort_vals_out[i]];
+}
+
+// ================================================================ permute (a6)
+template <int D>
+__global__ void gather_rows_kernel(const int* __restrict__ src, int64_t rows, const __nv_bfloat16* __restrict__ a,
+                                   __nv_bfloat16* __restrict__ a_out, const __nv_bfloat16* __restrict__ b,
+                                   __nv_bfloat16* __restrict__ b_out) {
+  constexpr int V = D / 8;  // uint4 per row
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / V;
+  const int c = (int)(gid % V);
+  if (row >= rows) return;
+  const int s = src[row];
+  if (s == -2) return;  // beyond the view's length: never read
+  uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
+  if (s >= 0) {
+    va = __ldg(reinterpret_cast<const uint4*>(a + (size_t)s * D) + c);
+    if (b) vb = __ldg(reinterpret_cast<const uint4*>(b + (size_t)s * D) + c);
+  }
+  reinterpret_cast<uint4*>(a_out + (size_t)row * D)[c] = va;
+  if (b) reinterpret_cast<uint4*>(b_out + (size_t)row * D)[c] = vb;
+}
+
+// ================================================================ merge (a8)
+__global__ void merge_kernel(IndexCtx C, int D, int h, int n_rows, __nv_bfloat16* __restrict__ o,
+                             float* __restrict__ lse) {
+  const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (warp_g >= n_rows) return;
+  const DHead hd = C.heads[h];
+  const int i = warp_g;
+  int pos, grp;
+  if (hd.qmod_view < 0) {
+    pos = i;
+    if (pos >= C.S) return;
+    grp = 0;
+  } else {
+    if (i >= C.info[MI_PADOFF + MAX_MOD]) return;
+    pos = C.modpos[i];
+    if (pos < 0) return;
+    grp = C.labels[pos];
+  }
+  const int gi = hd.sl_inst[grp];
+  if (gi < 0) return;
+  const DInst x = C.insts[h * MAX_INST + gi];
+  const GridRes g = C.gridres[x.grid_id];
+  const int coord = x.rank ? C.rank[pos] : pos;
+  const int r = coord % g.s;
+  if ((x.flags & GF_H) && r == g.p) return;  // written by the HROW pass
+  const float* o0 = C.part_o + (size_t)(hd.part_rows0 + i) * D;
+  float l0 = C.part_lse[hd.part_rows0 + i];
+  float l1 = -INFINITY;
+  const float* o1 = nullptr;
+  if (!(r == g.p && (x.flags & (GF_H | GF_V)))) {
+    ClassGeo cg;
+    cg.init(x.rank ? C.info[MI_CNT + x.qa] : C.S, g.s);
+    const int j = x.pad[0] + cg.classoff(r) + coord / g.s;
+    o1 = C.part_o + (size_t)j * D;
+    l1 = C.part_lse[j];
+  }
+  const float m = fmaxf(l0, l1);
+  const float w0 = (l0 == -INFINITY) ? 0.f : __expf(l0 - m);
+  const float w1 = (l1 == -INFINITY) ? 0.f : __expf(l1 - m);
+  const float tot = w0 + w1;
+  const float inv = tot > 0.f ? 1.f / tot : 0.f;
+  __nv_bfloat16* orow = o + ((size_t)h * C.S + pos) * D;
+  for (int d = lane * 2; d < D; d += 64) {
+    float a0 = o0[d] * w0, a1 = o0[d + 1] * w0;
+    if (o1) {
+      a0 += o1[d] * w1;
+      a1 += o1[d + 1] * w1;
+    }
+    *reinterpret_cast<__nv_bfloat162*>(orow + d) = __floats2bfloat162_rn(a0 * inv, a1 * inv);
+  }
+  if (lane == 0 && lse) lse[(size_t)h * C.S + pos] = tot > 0.f ? m + __logf(tot) : -INFINITY;
+}
+
+// ================================================================ launchers
+void launch_build_views(const IndexCtx& C, const int* qviews, int nq, const int* kviews, int nk, int64_t qrows,
+                        int64_t krows, cudaStream_t st) {
+  if (qrows > 0) build_views_kernel<<<(unsigned)((qrows + 255) / 256), 256, 0, st>>>(C, 0, qviews, nq, qrows);
+  if (krows > 0) build_views_kernel<<<(unsigned)((krows + 255) / 256), 256, 0, st>>>(C, 1, kviews, nk, krows);
+}
+void launch_inst_params(const IndexCtx& C, int n_total, cudaStream_t st) {
+  inst_params_kernel<<<(n_total + 127) / 128, 128, 0, st>>>(C, n_total);
+}
+void launch_items_count(const IndexCtx& C, cudaStream_t st) {
+  items_count_kernel<<<(C.n_slots + 127) / 128, 128, 0, st>>>(C);
+}
+void launch_items_fill(const IndexCtx& C, cudaStream_t st) {
+  items_fill_kernel<<<(C.n_slots + 127) / 128, 128, 0, st>>>(C);
+}
+void launch_items_gather(const IndexCtx& C, cudaStream_t st) {
+  items_gather_kernel<<<(C.n_slots + 127) / 128, 128, 0, st>>>(C);
+}
+void launch_gather(const int* src, int64_t rows, int D, const void* a, void* a_out, const void* b, void* b_out,
+                   cudaStream_t st) {
+  if (rows <= 0) return;
+  const int64_t threads = rows * (D / 8);
+  const unsigned grid = (unsigned)((threads + 255) / 256);
+  if (D == 128)
+    gather_rows_kernel<128><<<grid, 256, 0, st>>>(src, rows, (const __nv_bfloat16*)a, (__nv_bfloat16*)a_out,
+                                                  (const __nv_bfloat16*)b, (__nv_bfloat16*)b_out);
+  else
+    gather_rows_kernel<64><<<grid, 256, 0, st>>>(src, rows, (const __nv_bfloat16*)a, (__nv_bfloat16*)a_out,
+                                                 (const __nv_bfloat16*)b, (__nv_bfloat16*)b_out);
+}
+void launch_merge(const IndexCtx& C, int D, int h, int n_rows, void* o, float* lse, cudaStream_t st) {
+  if (n_rows <= 0) return;
+  const int threads = n_rows * 32;
+  merge_kernel<<<(threads + 255) / 256, 256, 0, st>>>(C, D, h, n_rows, (__nv_bfloat16*)o, lse);
+}
+
+}  // namespace mmi

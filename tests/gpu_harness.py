@@ -1,0 +1,158 @@
+"""Shared GPU-vs-oracle comparison helpers (imported by the -m gpu tests and
+__graft_entry__.smoke()).  Oracle = oracle/ (fp64 CPU); GPU = libmmi.so via the
+ctypes binding.  The two share only synth/ inputs."""
+from __future__ import annotations
+
+import struct
+from typing import Dict, List, Optional
+
+import numpy as np
+import torch
+
+from synth.config import (KIND_NONE, KIND_FULL, KIND_ASHAPE, KIND_VSLASH, KIND_GRID,
+                          BND_NONE, BND_K, BND_Q, BND_2D, MAX_MOD)
+from oracle.estimate import estimate_head
+from oracle.pipeline import run_head
+
+TOL_MAX, TOL_MEAN = 2e-2, 2e-3      # north_star attention tolerance (bf16 in, fp32 accumulate)
+
+
+def parse_export(words: torch.Tensor) -> Dict:
+    w = [int(x) for x in words.tolist()]
+    i = 0
+    n = w[i]; i += 1
+    insts = []
+    for _ in range(n):
+        kind, qa, kb, rank, s, p, valid = w[i:i + 7]; i += 7
+        J = struct.unpack("<d", struct.pack("<ii", w[i], w[i + 1]))[0]; i += 2
+        nV, nS = w[i], w[i + 1]; i += 2
+        V = np.array(w[i:i + nV], dtype=np.int64); i += nV
+        Sl = np.array(w[i:i + nS], dtype=np.int64); i += nS
+        insts.append(dict(kind=kind, qa=qa, kb=kb, rank=rank, s=s, p=p, valid=valid, J=J, V=V, Sl=Sl))
+    n_items = w[i]; tiles = struct.unpack("<q", struct.pack("<ii", w[i + 1], w[i + 2]))[0]; n_segs = w[i + 3]
+    return dict(insts=insts, n_items=n_items, tiles=tiles, n_segs=n_segs)
+
+
+def _flat_oracle_insts(cfg, idx) -> List[Dict]:
+    if cfg.boundary in (BND_NONE, BND_K):
+        return [idx["intra"][0]]
+    if cfg.boundary == BND_Q:
+        return [idx["intra"][m] for m in range(len(idx["intra"]))]
+    out = []
+    M = len(idx["pair"])
+    for a in range(M):
+        for b in range(M):
+            if cfg.pair[a][b].kind != KIND_NONE:
+                out.append(idx["pair"][a][b])
+    return out
+
+
+def _patterns(cfg, M) -> List:
+    if cfg.boundary in (BND_NONE, BND_K):
+        return [cfg.intra[0]]
+    if cfg.boundary == BND_Q:
+        return [cfg.intra[m] for m in range(M)]
+    return [cfg.pair[a][b] for a in range(M) for b in range(M) if cfg.pair[a][b].kind != KIND_NONE]
+
+
+def gpu_index_as_oracle(cfg, exp: Dict, M: int) -> Dict:
+    """Rebuild an oracle-style index dict from the GPU's exported index."""
+    pats = _patterns(cfg, M)
+    inst = []
+    for p, e in zip(pats, exp["insts"]):
+        if p.kind == KIND_GRID:
+            inst.append(dict(kind=KIND_GRID, s=e["s"], p=e["p"], h=p.use_hline, v=p.use_vline, sl=p.use_slash,
+                             sink=p.sink, local=p.local))
+        elif p.kind == KIND_VSLASH:
+            inst.append(dict(kind=KIND_VSLASH, V=e["V"], Sl=e["Sl"]))
+        elif p.kind == KIND_ASHAPE:
+            inst.append(dict(kind=KIND_ASHAPE, sink=p.sink, local=p.local))
+        else:
+            inst.append(dict(kind=p.kind))
+    if cfg.boundary in (BND_NONE, BND_K):
+        return dict(intra=inst)
+    if cfg.boundary == BND_Q:
+        return dict(intra=inst)
+    pair = [[dict(kind=KIND_NONE) for _ in range(M)] for _ in range(M)]
+    k = 0
+    for a in range(M):
+        for b in range(M):
+            if cfg.pair[a][b].kind != KIND_NONE:
+                pair[a][b] = inst[k]; k += 1
+    return dict(pair=pair)
+
+
+def compare_index(cfg, gpu_exp: Dict, oracle_idx: Dict, M: int) -> Dict:
+    """Bit-exact comparison of selected index sets; differences allowed only on
+    the oracle's near-tie candidates (reported)."""
+    rep = dict(exact=0, near=0, mismatch=[])
+    for p, g, o in zip(_patterns(cfg, M), gpu_exp["insts"], _flat_oracle_insts(cfg, oracle_idx)):
+        if p.kind == KIND_GRID:
+            if (g["s"], g["p"]) == (o["s"], o["p"]):
+                rep["exact"] += 1
+            elif (g["s"], g["p"]) in set(o.get("near", [])):
+                rep["near"] += 1
+            else:
+                rep["mismatch"].append(("grid", (g["s"], g["p"]), (o["s"], o["p"]), o["J"], g["J"]))
+        elif p.kind == KIND_VSLASH:
+            for key, nk in (("V", "near_v"), ("Sl", "near_s")):
+                a, b = set(g[key].tolist()), set(o[key].tolist())
+                diff = a ^ b
+                if not diff:
+                    rep["exact"] += 1
+                elif diff <= set(o.get(nk, [])):
+                    rep["near"] += 1
+                else:
+                    rep["mismatch"].append((key, sorted(diff)[:10], len(diff)))
+    return rep
+
+
+def run_gpu(wl, d, want_fp: bool = True):
+    from paper_2504_16083_b200 import SparsePrefill, mmi_export_index, mmi_sparse_fingerprint
+    pb = wl.problem
+    q, k, v = d["q"].cuda(), d["k"].cuda(), d["v"].cuda()
+    lab = torch.from_numpy(np.ascontiguousarray(d["labels"])).cuda()
+    sp = SparsePrefill(pb, wl.heads)
+    lse = torch.full((pb.n_heads, pb.seq_len), float("nan"), device="cuda")
+    o = torch.full((pb.n_heads, pb.seq_len, pb.head_dim), float("nan"), dtype=torch.bfloat16, device="cuda")
+    sp(q, k, v, lab, o=o, lse=lse)
+    torch.cuda.synchronize()
+    exps = [parse_export(mmi_export_index(pb, wl.heads, sp.ws, h)) for h in range(pb.n_heads)]
+    fp = None
+    if want_fp:
+        fpt = torch.zeros((pb.n_heads, pb.seq_len, 3), dtype=torch.int64, device="cuda")
+        mmi_sparse_fingerprint(pb, wl.heads, sp.ws, q, k, v, fpt)
+        torch.cuda.synchronize()
+        fp = fpt.cpu().numpy()
+    return dict(o=o.float().cpu().numpy(), lse=lse.cpu().numpy(), exp=exps, fp=fp)
+
+
+def check_head(wl, d, gpu, h: int, rows: Optional[np.ndarray] = None, check_index=True) -> Dict:
+    pb = wl.problem
+    G = pb.n_heads // pb.n_kv_heads
+    qh = d["q"][h].double().numpy()
+    kg = d["k"][h // G].double().numpy()
+    vg = d["v"][h // G].double().numpy()
+    cfg = wl.heads[h]
+    out = dict(head=h)
+    if check_index:
+        oidx = estimate_head(pb, cfg, qh, kg, d["labels"])
+        out["index"] = compare_index(cfg, gpu["exp"][h], oidx, pb.n_modalities)
+    gidx = gpu_index_as_oracle(cfg, gpu["exp"][h], pb.n_modalities)
+    r = run_head(pb, cfg, qh, kg, vg, d["labels"], rows=rows, index=gidx)
+    rr = r["rows"]
+    err = np.abs(gpu["o"][h][rr] - r["O"])
+    out["max_err"] = float(err.max())
+    out["mean_err"] = float(err.mean())
+    lse_g = gpu["lse"][h][rr]
+    out["lse_err"] = float(np.abs(lse_g - r["lse"]).max())
+    if gpu["fp"] is not None:
+        f = gpu["fp"][h][rr]
+        out["fp_count_ok"] = bool((f[:, 0] == r["count"]).all())
+        out["fp_sum_ok"] = bool((f[:, 1].astype(np.uint64) == r["sumj"]).all())
+        out["fp_sum2_ok"] = bool((f[:, 2].astype(np.uint64) == r["sumj2"]).all())
+        bad = np.nonzero(f[:, 0] != r["count"])[0]
+        out["fp_bad_rows"] = rr[bad[:5]].tolist()
+        out["fp_bad_detail"] = [(int(rr[b]), int(f[b, 0]), int(r["count"][b])) for b in bad[:5]]
+    out["tiles"] = gpu["exp"][h]["tiles"]
+    return out
