@@ -19,6 +19,8 @@
 using namespace mmi;
 
 static thread_local char g_err[1024];
+static long long* g_dbg = nullptr;  // debug-only per-item timestamps (mmi_debug_set_timestamps)
+extern "C" MMI_API void mmi_debug_set_timestamps(long long* p) { g_dbg = p; }
 
 static mmi_status fail(mmi_status st, const char* fmt, ...) {
   va_list ap;
@@ -234,6 +236,7 @@ static mmi_status run_sparse(const Plan& P, const mmi_problem* pb, void* ws, con
   A.scale_log2 = tau_of(pb) * 1.4426950408889634f;
   A.dense = 0;
   A.fingerprint = fp ? 1 : 0;
+  A.dbg = g_dbg;
   A.fp_out = fp;
   AttnLaunch L;
   L.q = q;
@@ -292,6 +295,7 @@ extern "C" mmi_status mmi_unpermute(const mmi_problem* pb, const mmi_head_config
   return MMI_OK;
 }
 
+
 extern "C" mmi_status mmi_dense_prefill(const mmi_problem* pb, const void* q, const void* k, const void* v, void* o,
                                         float* lse, mmi_stream_t stream) {
   mmi_status st = check_problem(pb);
@@ -305,6 +309,7 @@ extern "C" mmi_status mmi_dense_prefill(const mmi_problem* pb, const void* q, co
   A.D = pb->head_dim;
   A.scale_log2 = tau_of(pb) * 1.4426950408889634f;
   A.dense = 1;
+  A.dbg = g_dbg;
   A.o = o;
   A.lse = lse;
   AttnLaunch L;

@@ -11,12 +11,15 @@
 //
 // Warp roles (one CTA per SM, persistent, static round-robin over LPT-ordered
 // work items):
-//   warp 0     TMA producer: Q tile, K/V tiles (+ key positions for PRED tiles)
-//   warp 1     MMA issuer: S = Q K^T into TMEM (double buffered), O += P V
-//   warp 2     TMEM allocator
+//   warp 0     TMA Q loader (one Q tile per work item)
+//   warp 1     MMA issuer: S = Q K^T into TMEM (double buffered), O += P V; TMEM alloc
+//   warp 2     TMA K loader (K ring, + key positions / ranks for PRED tiles)
+//   warp 3     TMA V loader (V ring, decoupled from K so K runs ahead)
 //   warps 4-7  softmax / correction / epilogue, thread t owns query row t
-//              (TMEM lane t): tcgen05.ld S, predicate, exp2, P -> smem (bf16,
-//              128B-swizzled K-major UMMA layout), lazy O rescale in TMEM.
+//              (TMEM lane t): tcgen05.ld S, predicate mask, exp2, P (bf16) -> TMEM
+//              aliasing S (A operand of the P V tcgen05.mma), lazy O rescale in TMEM.
+// Work items are fetched dynamically (atomic counter) by warp 0 and broadcast to
+// the other roles through a 4-deep shared-memory ring.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -29,23 +32,31 @@
 
 namespace mmi {
 
-constexpr int NST = 2;             // K/V pipeline stages
 constexpr int NTHREADS = 256;
 constexpr float RESCALE_THRESH = 8.0f;  // lazy rescale: P <= 2^8 (log2 domain)
 
 template <int D>
+struct Cfg {
+  static constexpr int KST = (D == 128) ? 3 : 4;  // K ring stages
+  static constexpr int VST = (D == 128) ? 2 : 3;  // V ring stages
+};
+constexpr int SCHED_RING = 4;
+
+template <int D>
 struct Smem {
+  static constexpr int KST = Cfg<D>::KST, VST = Cfg<D>::VST;
   static constexpr int Q_BYTES = BLK * D * 2;
   static constexpr int KV_BYTES = BLK * D * 2;
-  static constexpr int P_BYTES = BLK * BLK * 2;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_P = OFF_Q + Q_BYTES;
-  static constexpr int OFF_K = OFF_P + P_BYTES;
-  static constexpr int OFF_V = OFF_K + NST * KV_BYTES;
-  static constexpr int OFF_KPOS = OFF_V + NST * KV_BYTES;
-  static constexpr int OFF_KRANK = OFF_KPOS + NST * BLK * 4;
-  static constexpr int OFF_BAR = OFF_KRANK + NST * BLK * 4;
-  static constexpr int N_BAR = 2 + 2 * NST + 4 + 4;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
+  static constexpr int OFF_KPOS = OFF_V + VST * KV_BYTES;
+  static constexpr int OFF_KRANK = OFF_KPOS + KST * BLK * 4;
+  static constexpr int OFF_SCHED = OFF_KRANK + KST * BLK * 4;
+  static constexpr int OFF_BAR = OFF_SCHED + 64;
+  // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2] p_full[2]
+  // pv_done o_full o_empty sched_full[R] sched_empty[R]
+  static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 4 + 3 + 2 * SCHED_RING;
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
   static constexpr int TOTAL = OFF_TMEM + 16;
   static constexpr int ALLOC = TOTAL + 1024;  // alignment slack
@@ -93,6 +104,22 @@ __device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx) {
   v.row_mod = w.row_mod;
   v.rb = 0;
   return v;
+}
+
+// sets bits [lo, hi] (clipped to [0, 127]) of a 128-bit mask
+__device__ __forceinline__ void range_mask(uint32_t (&mw)[4], int lo, int hi) {
+  lo = max(lo, 0);
+  hi = min(hi, BLK - 1);
+  if (hi < lo) return;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int a = max(lo - 32 * w, 0), b = min(hi - 32 * w, 31);
+    if (b >= a) {
+      const uint32_t hiMask = (b == 31) ? 0xffffffffu : ((1u << (b + 1)) - 1u);
+      const uint32_t loMask = (1u << a) - 1u;
+      mw[w] |= hiMask & ~loMask;
+    }
+  }
 }
 
 struct TileInfo {
@@ -143,22 +170,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const __grid_constant__ CUtensorMap tmVo, const __grid_constant__ CUtensorMap tmVg,
                 const AttnParams P) {
   using L = Smem<D>;
+  constexpr int KST = L::KST, VST = L::VST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
-  uint64_t* kv_full = bars + 2;
-  uint64_t* kv_empty = bars + 2 + NST;
-  uint64_t* s_full = bars + 2 + 2 * NST;   // [2]
-  uint64_t* s_empty = s_full + 2;          // [2]
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* p_empty = p_full + 1;
-  uint64_t* o_full = p_empty + 1;
+  uint64_t* k_full = bars + 2;
+  uint64_t* k_empty = k_full + KST;
+  uint64_t* v_full = k_empty + KST;
+  uint64_t* v_empty = v_full + VST;
+  uint64_t* s_full = v_empty + VST;   // [2] S buffer written by the MMA
+  uint64_t* p_full = s_full + 2;      // [2] P (bf16, aliasing S in TMEM) written by the softmax
+  uint64_t* pv_done = p_full + 2;     // one phase per P V MMA
+  uint64_t* o_full = pv_done + 1;
   uint64_t* o_empty = o_full + 1;
+  uint64_t* sched_full = o_empty + 1;
+  uint64_t* sched_empty = sched_full + SCHED_RING;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
   int32_t* kpos_s = reinterpret_cast<int32_t*>(smem + L::OFF_KPOS);
   int32_t* krank_s = reinterpret_cast<int32_t*>(smem + L::OFF_KRANK);
+  volatile int32_t* sched_ring = reinterpret_cast<volatile int32_t*>(smem + L::OFF_SCHED);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -166,21 +198,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(kv_full + i, 1);
-      mbar_init(kv_empty + i, 1);
+    for (int i = 0; i < KST; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1 + 4);  // S-MMA commit + one arrival per softmax warp (key coords consumed)
+    }
+    for (int i = 0; i < VST; ++i) {
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
-      mbar_init(s_empty + i, 128);
+      mbar_init(p_full + i, 128);
     }
-    mbar_init(p_full, 128);
-    mbar_init(p_empty, 1);
+    mbar_init(pv_done, 1);
     mbar_init(o_full, 1);
     mbar_init(o_empty, 128);
+    for (int i = 0; i < SCHED_RING; ++i) {
+      mbar_init(sched_full + i, 1);
+      mbar_init(sched_empty + i, 3 + 4);  // K loader, V loader, MMA, 4 softmax warps
+    }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_holder);
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQo);
     tma_prefetch_desc(&tmQg);
@@ -197,137 +236,165 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tO = tmem + 256;
 
   const int n_items = P.dense ? P.H * ((P.S + BLK - 1) / BLK) : P.n_items;
+  // consumer side of the work-item ring
+  auto fetch = [&](int i) -> int {
+    const int slot = i % SCHED_RING;
+    mbar_wait(sched_full + slot, (i / SCHED_RING) & 1);
+    return sched_ring[slot];
+  };
 
   if (warp == 0) {
-    // ======================= TMA producer =======================
+    // ======================= scheduler + Q loader =======================
     if (elect_one()) {
-      int stage = 0;
-      uint32_t kv_phase = 0, q_phase = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      uint32_t q_phase = 0;
+      for (int i = 0;; ++i) {
+        const int slot = i % SCHED_RING;
+        mbar_wait(sched_empty + slot, ((i / SCHED_RING) & 1) ^ 1);
+        int idx = (i == 0) ? (int)blockIdx.x : (int)gridDim.x + (int)atomicAdd(P.sched, 1u);
+        if (idx >= n_items) idx = -1;
+        sched_ring[slot] = idx;
+        mbar_arrive(sched_full + slot);
+        if (idx < 0) break;
         const ItemView it = load_item(P, idx);
         if (it.n_tiles <= 0) continue;
+        if (P.dbg) P.dbg[idx * 8 + 0] = gtimer();
         mbar_wait(q_empty, q_phase ^ 1);
+        if (P.dbg) P.dbg[idx * 8 + 1] = gtimer();
         q_phase ^= 1;
         mbar_arrive_expect_tx(q_full, L::Q_BYTES);
         const CUtensorMap* tq = it.q_gathered ? &tmQg : &tmQo;
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
           tma_load_2d(smem + L::OFF_Q + c * (BLK * 128), tq, q_full, c * 64, it.q_row0);
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // ======================= K loader (warp 2) / V loader (warp 3) =======================
+    const bool is_k = (warp == 2);
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const int NS = is_k ? KST : VST;
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      for (int i = 0;; ++i) {
+        const int idx = fetch(i);
+        mbar_arrive(sched_empty + i % SCHED_RING);
+        if (idx < 0) break;
+        const ItemView it = load_item(P, idx);
+        if (it.n_tiles <= 0) continue;
         SegIter si;
         si.init(P, it);
         for (int t = 0; t < it.n_tiles; ++t) {
           const TileInfo e = si.next(P, it);
-          const uint32_t space = e.space, pred = e.pred, rank = e.rmode;
-          mbar_wait(kv_empty + stage, kv_phase ^ 1);
-          uint32_t bytes = 2 * L::KV_BYTES;
-          const bool cp_pos = (pred || P.fingerprint) && space;
-          const bool cp_rank = pred && space && rank;
+          mbar_wait(empty + stage, phase ^ 1);
+          uint32_t bytes = L::KV_BYTES;
+          const bool cp_pos = is_k && (e.pred || P.fingerprint) && e.space;
+          const bool cp_rank = is_k && e.pred && e.space && e.rmode;
           if (cp_pos) bytes += BLK * 4;
           if (cp_rank) bytes += BLK * 4;
-          mbar_arrive_expect_tx(kv_full + stage, bytes);
-          const CUtensorMap* tk = space ? &tmKg : &tmKo;
-          const CUtensorMap* tv = space ? &tmVg : &tmVo;
-          uint8_t* ks = smem + L::OFF_K + stage * L::KV_BYTES;
-          uint8_t* vs = smem + L::OFF_V + stage * L::KV_BYTES;
+          mbar_arrive_expect_tx(full + stage, bytes);
+          const CUtensorMap* tm = is_k ? (e.space ? &tmKg : &tmKo) : (e.space ? &tmVg : &tmVo);
+          uint8_t* dst = smem + (is_k ? L::OFF_K : L::OFF_V) + stage * L::KV_BYTES;
 #pragma unroll
-          for (int c = 0; c < D / 64; ++c) {
-            tma_load_2d(ks + c * (BLK * 128), tk, kv_full + stage, c * 64, e.krow);
-            tma_load_2d(vs + c * (BLK * 128), tv, kv_full + stage, c * 64, e.krow);
-          }
-          if (cp_pos) bulk_load(kpos_s + stage * BLK, P.kg_pos + e.krow, BLK * 4, kv_full + stage);
-          if (cp_rank) bulk_load(krank_s + stage * BLK, P.kg_rank + e.krow, BLK * 4, kv_full + stage);
-          if (++stage == NST) {
+          for (int c = 0; c < D / 64; ++c) tma_load_2d(dst + c * (BLK * 128), tm, full + stage, c * 64, e.krow);
+          if (cp_pos) bulk_load(kpos_s + stage * BLK, P.kg_pos + e.krow, BLK * 4, full + stage);
+          if (cp_rank) bulk_load(krank_s + stage * BLK, P.kg_rank + e.krow, BLK * 4, full + stage);
+          if (++stage == NS) {
             stage = 0;
-            kv_phase ^= 1;
+            phase ^= 1;
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer =======================
-    constexpr uint32_t IDESC_S = idesc_bf16(128, 128, 0);
-    constexpr uint32_t IDESC_O = idesc_bf16(128, D, 1);
-    const uint32_t q_base = smem_u32(smem + L::OFF_Q);
-    const uint32_t p_base = smem_u32(smem + L::OFF_P);
-    const uint32_t k_base = smem_u32(smem + L::OFF_K);
-    const uint32_t v_base = smem_u32(smem + L::OFF_V);
-    int stage = 0;
-    uint32_t kv_phase = 0, q_phase = 0, p_phase = 0, o_phase = 0;
-    uint32_t s_phase[2] = {0, 0};
-    int sbuf = 0;
-    const bool leader = elect_one();
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
-      const ItemView it = load_item(P, idx);
-      if (it.n_tiles <= 0) continue;
-      mbar_wait(q_full, q_phase);
-      q_phase ^= 1;
-      tc_fence_after();
-      int prev_stage = -1;
-      for (int t = 0; t <= it.n_tiles; ++t) {
-        int cur_stage = stage;
-        if (t < it.n_tiles) {
-          // S[sbuf] = Q K_t^T
-          mbar_wait(kv_full + stage, kv_phase);
-          mbar_wait(s_empty + sbuf, s_phase[sbuf] ^ 1);
-          tc_fence_after();
-          if (leader) {
+    // ======================= MMA issuer (one thread) =======================
+    if (elect_one()) {
+      constexpr uint32_t IDESC_S = idesc_bf16(128, 128, 0);
+      constexpr uint32_t IDESC_O = idesc_bf16(128, D, 1);
+      const uint32_t q_base = smem_u32(smem + L::OFF_Q);
+      const uint32_t k_base = smem_u32(smem + L::OFF_K);
+      const uint32_t v_base = smem_u32(smem + L::OFF_V);
+      int ks = 0, vs = 0, sb = 0;
+      uint32_t k_phase = 0, v_phase = 0, q_phase = 0, o_phase = 0;
+      uint32_t p_phase[2] = {0, 0};
+      for (int i = 0;; ++i) {
+        const int idx = fetch(i);
+        mbar_arrive(sched_empty + i % SCHED_RING);
+        if (idx < 0) break;
+        const ItemView it = load_item(P, idx);
+        if (it.n_tiles <= 0) continue;
+        mbar_wait(q_full, q_phase);
+        if (P.dbg) P.dbg[idx * 8 + 2] = gtimer();
+        q_phase ^= 1;
+        tc_fence_after();
+        int sb_prev = 0;
+        for (int t = 0; t <= it.n_tiles; ++t) {
+          const int sb_cur = sb;
+          if (t < it.n_tiles) {
+            // S[sb] = Q K_t^T.  The buffer's previous P (tile t-2) was consumed by a P V issued
+            // before this MMA; tcgen05.mma executes in issue order.
+            mbar_wait(k_full + ks, k_phase);
+            tc_fence_after();
 #pragma unroll
             for (int k = 0; k < D / 16; ++k) {
               const uint32_t off = (k / 4) * (BLK * 128) + (k % 4) * 32;
               const uint64_t ad = smem_desc(q_base + off, 16, 1024, 2);
-              const uint64_t bd = smem_desc(k_base + stage * L::KV_BYTES + off, 16, 1024, 2);
-              umma_ss(tS[sbuf], ad, bd, IDESC_S, k > 0 ? 1u : 0u);
+              const uint64_t bd = smem_desc(k_base + ks * L::KV_BYTES + off, 16, 1024, 2);
+              umma_ss(tS[sb], ad, bd, IDESC_S, k > 0 ? 1u : 0u);
             }
-            umma_commit(s_full + sbuf);
+            umma_commit(s_full + sb);
+            umma_commit(k_empty + ks);
             if (t == it.n_tiles - 1) umma_commit(q_empty);
+            sb ^= 1;
+            if (++ks == KST) {
+              ks = 0;
+              k_phase ^= 1;
+            }
           }
-          __syncwarp();
-          s_phase[sbuf] ^= 1;
-          sbuf ^= 1;
-          if (++stage == NST) {
-            stage = 0;
-            kv_phase ^= 1;
-          }
-        }
-        if (t >= 1) {
-          // O += P_{t-1} V_{t-1}
-          mbar_wait(p_full, p_phase);
-          p_phase ^= 1;
-          if (t == 1) {
-            mbar_wait(o_empty, o_phase ^ 1);  // previous item's epilogue has read O
-          }
-          tc_fence_after();
-          if (leader) {
+          if (t >= 1) {
+            // O += P_{t-1} V_{t-1}, P read from TMEM (aliasing S buffer sb_prev)
+            mbar_wait(p_full + sb_prev, p_phase[sb_prev]);
+            p_phase[sb_prev] ^= 1;
+            if (t == 1) mbar_wait(o_empty, o_phase ^ 1);  // previous item's epilogue has read O
+            mbar_wait(v_full + vs, v_phase);
+            tc_fence_after();
 #pragma unroll
             for (int k = 0; k < BLK / 16; ++k) {
-              const uint32_t aoff = (k / 4) * (BLK * 128) + (k % 4) * 32;
-              const uint64_t ad = smem_desc(p_base + aoff, 16, 1024, 2);
-              const uint64_t bd = smem_desc(v_base + prev_stage * L::KV_BYTES + k * 2048, BLK * 128, 1024, 2);
-              umma_ss(tO, ad, bd, IDESC_O, (t > 1 || k > 0) ? 1u : 0u);
+              const uint64_t bd = smem_desc(v_base + vs * L::KV_BYTES + k * 2048, BLK * 128, 1024, 2);
+              umma_ts(tO, tS[sb_prev] + k * 8, bd, IDESC_O, (t > 1 || k > 0) ? 1u : 0u);
             }
-            umma_commit(kv_empty + prev_stage);
-            umma_commit(p_empty);
+            umma_commit(v_empty + vs);
+            umma_commit(pv_done);
             if (t == it.n_tiles) umma_commit(o_full);
+            if (++vs == VST) {
+              vs = 0;
+              v_phase ^= 1;
+            }
           }
-          __syncwarp();
+          sb_prev = sb_cur;
         }
-        prev_stage = cur_stage;
+        o_phase ^= 1;
       }
-      o_phase ^= 1;
     }
   } else if (warp >= 4) {
-    // ======================= softmax / epilogue =======================
+    // ======================= softmax / correction / epilogue =======================
     const int row = threadIdx.x - 128;                 // TMEM lane == query row
     const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
-    const uint32_t p_base = smem_u32(smem + L::OFF_P);
-    int stage = 0;
-    uint32_t kv_phase = 0, p_phase = 0, o_phase = 0;
+    int stage = 0;  // K ring stage (key coordinates)
+    uint32_t kv_phase = 0, o_phase = 0;
     uint32_t s_phase[2] = {0, 0};
     int sbuf = 0;
+    long long pv_count = 0;  // P V MMAs issued so far by this CTA (phase index of pv_done)
     const int G = P.H / P.Hkv;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    for (int i = 0;; ++i) {
+      const int idx = fetch(i);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sched_empty + i % SCHED_RING);
+      if (idx < 0) break;
       const ItemView it = load_item(P, idx);
       if (it.n_tiles <= 0) continue;  // empty slot: nothing to compute or write
+      if (P.dbg && row == 0) P.dbg[idx * 8 + 3] = gtimer();
       // row identity
       int xpos, xrank;
       if (it.q_gathered) {
@@ -353,6 +420,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const TileInfo e = si.next(P, it);
         const uint32_t space = e.space, pred = e.pred, role = e.role, rmode = e.rmode, inst = e.inst;
         mbar_wait(s_full + sbuf, s_phase[sbuf]);
+        if (P.dbg && row == 0 && t == 0) P.dbg[idx * 8 + 7] = gtimer();
         s_phase[sbuf] ^= 1;
         tc_fence_after();
         float s[BLK];
@@ -364,68 +432,98 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(r[j]) * P.scale_log2;
         }
-        tc_fence_before();
-        mbar_arrive(s_empty + sbuf);
-        sbuf ^= 1;
-        if (pred || (P.fingerprint && space)) mbar_wait(kv_full + stage, kv_phase);
-        if (pred) {
-          // key coordinates for this tile
-          int sink = 0, local = 0;
-          const uint32_t* sl_bits = nullptr;
-          const uint32_t* vm_bits = nullptr;
-          if (!P.dense) {
-            const InstParam ip = P.insts[it.inst_base + inst];
-            sink = ip.sink;
-            local = ip.local;
-            if (ip.slash_word >= 0) sl_bits = P.bits + ip.slash_word;
-            if (ip.vmask_word >= 0) vm_bits = P.bits + ip.vmask_word;
-          }
-          const int x = rmode ? xrank : xpos;
-          const int kbase = e.krow - kv * P.S;
-#pragma unroll
-          for (int c = 0; c < BLK; ++c) {
-            int ypos, y;
-            if (space) {
-              ypos = kpos_s[stage * BLK + c];
-              y = rmode ? krank_s[stage * BLK + c] : ypos;
+        if (pred || (P.fingerprint && space)) mbar_wait(k_full + stage, kv_phase);
+        if (pred || P.fingerprint) {
+          // admitted-key bit mask of this tile (bit c <-> key c), then one unrolled select
+          uint32_t mw[4] = {0u, 0u, 0u, 0u};
+          if (valid) {
+            const int kbase = e.krow - kv * P.S;
+            if (!pred) {
+              range_mask(mw, 0, BLK - 1);
+            } else if (!space) {
+              // original K: contiguous positions kbase + c, coordinates == positions
+              const int hi = xpos - kbase;  // causal: c <= hi
+              int sink = 0, local = 0;
+              if (!P.dense && role != R_TRUE) {
+                const InstParam ip = P.insts[it.inst_base + inst];
+                sink = ip.sink;
+                local = ip.local;
+              }
+              if (role == R_TRUE) {
+                range_mask(mw, 0, hi);
+              } else if (role == R_A) {
+                range_mask(mw, 0, min(hi, sink - 1 - kbase));
+                range_mask(mw, max(0, xpos - local + 1 - kbase), hi);
+              } else if (role == R_NOTA) {
+                range_mask(mw, max(0, sink - kbase), min(hi, xpos - local - kbase));
+              } else {
+                const InstParam ip = P.insts[it.inst_base + inst];
+                const uint32_t* sl_bits = P.bits + ip.slash_word;
+                const uint32_t* vm_bits = P.bits + ip.vmask_word;
+                const int x = rmode ? xrank : xpos;
+                for (int c = 0; c <= min(hi, BLK - 1); ++c) {
+                  const int y = kbase + c, o = x - y;
+                  const bool ok = ((sl_bits[o >> 5] >> (o & 31)) & 1u) && !((vm_bits[y >> 5] >> (y & 31)) & 1u);
+                  mw[c >> 5] |= (uint32_t)ok << (c & 31);
+                }
+              }
             } else {
-              ypos = kbase + c;
-              y = ypos;
-            }
-            bool ok = valid && (ypos <= xpos);
-            if (role == R_A) {
-              ok = ok && ((y < sink) || (x - y < local));
-            } else if (role == R_NOTA) {
-              ok = ok && !((y < sink) || (x - y < local));
-            } else if (role == R_VSSL) {
-              if (ok) {
-                const int o = x - y;
-                const bool in_sl = (sl_bits[o >> 5] >> (o & 31)) & 1u;
-                const bool in_v = (vm_bits[y >> 5] >> (y & 31)) & 1u;
-                ok = in_sl && !in_v;
+              // gathered K view: per-key positions / ranks from the stage
+              int sink = 0, local = 0;
+              const uint32_t* sl_bits = nullptr;
+              const uint32_t* vm_bits = nullptr;
+              if (!P.dense) {
+                const InstParam ip = P.insts[it.inst_base + inst];
+                sink = ip.sink;
+                local = ip.local;
+                if (ip.slash_word >= 0) sl_bits = P.bits + ip.slash_word;
+                if (ip.vmask_word >= 0) vm_bits = P.bits + ip.vmask_word;
+              }
+              const int x = rmode ? xrank : xpos;
+              const int* kp = kpos_s + stage * BLK;
+              const int* kr = krank_s + stage * BLK;
+#pragma unroll 4
+              for (int c = 0; c < BLK; ++c) {
+                const int ypos = kp[c];
+                const int y = rmode ? kr[c] : ypos;
+                bool ok = ypos <= xpos;
+                if (role == R_A)
+                  ok = ok && ((y < sink) || (x - y < local));
+                else if (role == R_NOTA)
+                  ok = ok && (y >= sink) && (x - y >= local);
+                else if (role == R_VSSL && ok) {
+                  const int o = x - y;
+                  ok = ((sl_bits[o >> 5] >> (o & 31)) & 1u) && !((vm_bits[y >> 5] >> (y & 31)) & 1u);
+                }
+                mw[c >> 5] |= (uint32_t)ok << (c & 31);
               }
             }
-            if (!ok) s[c] = -INFINITY;
-            if (P.fingerprint && ok) {
-              fp_cnt += 1;
-              fp_s1 += ypos;
-              fp_s2 += (long long)ypos * ypos;
+            if (P.fingerprint) {
+#pragma unroll 1
+              for (int w = 0; w < 4; ++w) {
+                uint32_t bitsw = mw[w];
+                while (bitsw) {
+                  const int c = w * 32 + __ffs(bitsw) - 1;
+                  bitsw &= bitsw - 1;
+                  const long long ypos = space ? kpos_s[stage * BLK + c] : kbase + c;
+                  fp_cnt += 1;
+                  fp_s1 += ypos;
+                  fp_s2 += ypos * ypos;
+                }
+              }
             }
           }
-        } else if (P.fingerprint && valid) {
-          const int kbase = e.krow - kv * P.S;
-          for (int c = 0; c < BLK; ++c) {
-            const int ypos = space ? kpos_s[stage * BLK + c] : kbase + c;
-            fp_cnt += 1;
-            fp_s1 += ypos;
-            fp_s2 += (long long)ypos * ypos;
-          }
+#pragma unroll
+          for (int c = 0; c < BLK; ++c)
+            if (!((mw[c >> 5] >> (c & 31)) & 1u)) s[c] = -INFINITY;
         }
-        if (++stage == NST) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(k_empty + stage);  // key coordinates of this stage consumed
+        if (++stage == KST) {
           stage = 0;
           kv_phase ^= 1;
         }
-        // ---- online softmax (log2 domain) ----
+        // ---- online softmax (log2 domain), lazy rescale ----
         float mt = -INFINITY;
 #pragma unroll
         for (int c = 0; c < BLK; ++c) mt = fmaxf(mt, s[c]);
@@ -447,11 +545,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           pk[c / 2] = pack_bf16(p0, p1);
         }
         l_sum = l_sum * alpha + ls;
-        // P buffer and O are free once the previous P V has completed
-        mbar_wait(p_empty, p_phase ^ 1);
-        p_phase ^= 1;
-        tc_fence_after();
+        // O correction: only when the running max moved; needs the previous P V complete
         if (t > 0 && __any_sync(0xffffffffu, rescale)) {
+          mbar_wait(pv_done, (uint32_t)((pv_count + t - 1) & 1));
+          tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t r[32];
@@ -461,32 +558,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
             tmem_st32(tO + lane_off + c * 32, r);
           }
-          tmem_wait_st();
         }
-        // P row -> smem, K-major SW128: chunk = key/64, 16B unit u at (u ^ (row & 7))
-#pragma unroll
-        for (int u = 0; u < BLK / 8; ++u) {
-          const int chunk = u / 8, uu = u % 8;
-          const uint32_t addr = p_base + chunk * (BLK * 128) + row * 128 + ((uu ^ (row & 7)) << 4);
-          st_shared_v4(addr, pk[u * 4 + 0], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
-        }
-        fence_proxy_async_smem();
+        // P (bf16 pairs) -> TMEM columns [0, 64) of this S buffer: the A operand of P V
+        tmem_st32(tS[sbuf] + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        tmem_st32(tS[sbuf] + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(p_full);
+        mbar_arrive(p_full + sbuf);
+        sbuf ^= 1;
       }
+      pv_count += it.n_tiles;
       // ---- epilogue ----
-      if (it.n_tiles > 0) {
-        mbar_wait(o_full, o_phase);
-        o_phase ^= 1;
-        tc_fence_after();
-      }
+      if (P.dbg && row == 0) P.dbg[idx * 8 + 4] = gtimer();
+      mbar_wait(o_full, o_phase);
+      o_phase ^= 1;
+      tc_fence_after();
+      if (P.dbg && row == 0) P.dbg[idx * 8 + 5] = gtimer();
       const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
       const float lse_v = l_sum > 0.f ? (m_used + __log2f(l_sum)) * 0.6931471805599453f : -INFINITY;
       if (P.fingerprint) {
-        if (it.n_tiles > 0) {
-          tc_fence_before();
-          mbar_arrive(o_empty);
-        }
+        tc_fence_before();
+        mbar_arrive(o_empty);
         if (write) {
           long long* f = reinterpret_cast<long long*>(P.fp_out) + 3ll * ((long long)it.head * P.S + xpos);
           atomicAdd(reinterpret_cast<unsigned long long*>(f + 0), (unsigned long long)fp_cnt);
@@ -500,12 +592,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
-          if (it.n_tiles > 0) {
-            tmem_ld32(tO + lane_off + c * 32, r);
-            tmem_wait_ld();
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = 0u;
+          tmem_ld32(tO + lane_off + c * 32, r);
+          tmem_wait_ld();
+          if (c == D / 32 - 1) {
+            tc_fence_before();
+            mbar_arrive(o_empty);  // O fully in registers: the next item's first P V may start
           }
           if (write) {
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
@@ -526,12 +617,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
-          if (it.n_tiles > 0) {
-            tmem_ld32(tO + lane_off + c * 32, r);
-            tmem_wait_ld();
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = 0u;
+          tmem_ld32(tO + lane_off + c * 32, r);
+          tmem_wait_ld();
+          if (c == D / 32 - 1) {
+            tc_fence_before();
+            mbar_arrive(o_empty);
           }
           float4* dst = reinterpret_cast<float4*>(prow + c * 32);
 #pragma unroll
@@ -541,15 +631,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         P.part_lse[it.out_row0 + row] = valid ? lse_v : -INFINITY;
       }
-      if (it.n_tiles > 0) {
-        tc_fence_before();
-        mbar_arrive(o_empty);
-      }
+      if (P.dbg && row == 0) P.dbg[idx * 8 + 6] = gtimer();
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -588,6 +675,9 @@ int make_tmap_rows(CUtensorMap* m, const void* base, long long rows, int D) {
 }
 
 static int g_num_sms = 0;
+// work-item counters for launches without a workspace (dense comparator); rotating slots
+__device__ unsigned int g_sched_counters[64];
+static unsigned g_sched_slot = 0;
 
 cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hint, cudaStream_t stream,
                         int* tmap_err) {
@@ -609,14 +699,21 @@ cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hi
   int grid = g_num_sms;
   if (n_items_hint > 0 && n_items_hint < grid) grid = n_items_hint;
   if (grid <= 0) return cudaSuccess;
+  AttnParams Pl = P;
+  if (!Pl.sched) {
+    unsigned int* base = nullptr;
+    cudaGetSymbolAddress(reinterpret_cast<void**>(&base), g_sched_counters);
+    Pl.sched = base + (g_sched_slot++ % 64);
+  }
+  cudaMemsetAsync(Pl.sched, 0, sizeof(unsigned int), stream);
   if (P.D == 128) {
     auto kfn = attn_kernel<128>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::ALLOC);
-    kfn<<<grid, NTHREADS, Smem<128>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], P);
+    kfn<<<grid, NTHREADS, Smem<128>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], Pl);
   } else {
     auto kfn = attn_kernel<64>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<64>::ALLOC);
-    kfn<<<grid, NTHREADS, Smem<64>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], P);
+    kfn<<<grid, NTHREADS, Smem<64>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], Pl);
   }
   return cudaGetLastError();
 }

@@ -17,6 +17,8 @@
 
 namespace mmi {
 
+constexpr int LONG_ITEM_TILES = 48;
+
 __device__ __forceinline__ int pad128d(int x) { return (x + BLK - 1) / BLK * BLK; }
 __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
 
@@ -528,6 +530,7 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
       W.out_mode = OUT_PARTIAL;
       W.out_row0 = hd.part_rows0 + b * BLK;
     }
+    W.pad[0] = R.xp_lo;
     for (int ii = 0; ii < hd.n_inst; ++ii) {
       const DInst x = C.insts[I.h * MAX_INST + ii];
       if (x.qa >= 0 && x.qa != grp) continue;
@@ -572,6 +575,7 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
       R.xp_hi = c_hi;
       R.xr_lo = R.xr_hi = 0;
     }
+    W.pad[0] = R.xp_lo;
     if (ps.pass == PASS_HROW) {
       // the whole causal row of the pattern's key base (role TRUE)
       DInst xf = x;
@@ -632,7 +636,14 @@ __global__ void items_fill_kernel(IndexCtx C) {
   W.n_segs = E.n_segs;
   W.n_tiles = E.n_tiles;
   C.items[slot] = W;
-  C.sort_keys[slot] = E.n_tiles;
+  // work order: long items first by length (LPT); short items by position then head,
+  // so that concurrently running CTAs share the key tiles of a KV group in L2.
+  int key = 0;
+  if (E.n_tiles >= LONG_ITEM_TILES)
+    key = 0x40000000 + E.n_tiles;
+  else if (E.n_tiles > 0)
+    key = 0x3FFFFFFF - ((W.pad[0] / BLK) * 64 + (W.head & 63));
+  C.sort_keys[slot] = key;
   C.sort_vals[slot] = slot;
 }
 

@@ -76,6 +76,8 @@ struct AttnParams {
   int32_t dense;            // 1 => implicit dense causal items (same-build comparator)
   int32_t fingerprint;      // 1 => accumulate per-row admitted-key fingerprints instead of attention
   int64_t* fp_out;          // [H, S, 3] count, sum pos, sum pos^2 (fingerprint mode)
+  long long* dbg;           // optional per-item timestamps (debug only)
+  unsigned int* sched;      // work-item counter (zeroed before the launch)
 };
 
 struct AttnLaunch {

@@ -182,24 +182,54 @@ def mmi_export_index(pb, cfgs, ws, head: int, stream=None) -> torch.Tensor:
 
 # ------------------------------------------------------------------ convenience
 class SparsePrefill:
-    """One layer's sparse pre-fill: owns the workspace, runs the four C-ABI calls."""
+    """One layer's sparse pre-fill: owns the workspace and the marshalled C
+    structs; each call runs the four C-ABI calls on the current stream."""
 
     def __init__(self, pb: Problem, cfgs: List[HeadConfig], device="cuda"):
         self.pb, self.cfgs = pb, list(cfgs)
-        nbytes = mmi_workspace_bytes(pb, self.cfgs)
+        self.c_pb = to_c_problem(pb)
+        self.c_cfg = to_c_configs(self.cfgs)
+        nbytes = int(lib().mmi_workspace_bytes(ctypes.byref(self.c_pb), self.c_cfg))
         if nbytes == 0:
             raise MMIError(1, lib().mmi_last_error().decode())
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.ws_bytes = nbytes
+
+    def estimate(self, q, k, modality, stream=None):
+        _check(lib().mmi_estimate_index(ctypes.byref(self.c_pb), self.c_cfg, _ptr(q), _ptr(k), _ptr(modality),
+                                        _ptr(self.ws), self.ws_bytes, _stream(stream)))
+
+    def permute(self, q, k, v, stream=None):
+        _check(lib().mmi_permute(ctypes.byref(self.c_pb), self.c_cfg, _ptr(self.ws), self.ws_bytes, _ptr(q), _ptr(k),
+                                 _ptr(v), _stream(stream)))
+
+    def sparse(self, q, k, v, o, lse=None, stream=None):
+        _check(lib().mmi_sparse_prefill(ctypes.byref(self.c_pb), self.c_cfg, _ptr(self.ws), self.ws_bytes, _ptr(q),
+                                        _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _stream(stream)))
+
+    def unpermute(self, o, lse=None, stream=None):
+        _check(lib().mmi_unpermute(ctypes.byref(self.c_pb), self.c_cfg, _ptr(self.ws), self.ws_bytes, _ptr(o),
+                                   _ptr(lse), _stream(stream)))
 
     def __call__(self, q, k, v, modality, o=None, lse=None, stream=None):
         pb = self.pb
+        _need_cuda(q, k, v, modality, o, lse)
         if o is None:
             o = torch.empty((pb.n_heads, pb.seq_len, pb.head_dim), dtype=torch.bfloat16, device=q.device)
-        mmi_estimate_index(pb, self.cfgs, q, k, modality, self.ws, stream)
-        mmi_permute(pb, self.cfgs, self.ws, q, k, v, stream)
-        mmi_sparse_prefill(pb, self.cfgs, self.ws, q, k, v, o, lse, stream)
-        mmi_unpermute(pb, self.cfgs, self.ws, o, lse, stream)
+        self.estimate(q, k, modality, stream)
+        self.permute(q, k, v, stream)
+        self.sparse(q, k, v, o, lse, stream)
+        self.unpermute(o, lse, stream)
         return o
+
+    def total_tiles(self) -> int:
+        """Computed key tiles of the last index (TEST/bench helper: synchronises)."""
+        import struct
+        t = 0
+        for h in range(self.pb.n_heads):
+            w = mmi_export_index(self.pb, self.cfgs, self.ws, h).tolist()
+            t += struct.unpack("<q", struct.pack("<ii", w[-3], w[-2]))[0]
+        return t
 
 
 def dense_prefill(pb: Problem, q, k, v, o=None, lse=None, stream=None):
@@ -207,3 +237,33 @@ def dense_prefill(pb: Problem, q, k, v, o=None, lse=None, stream=None):
         o = torch.empty((pb.n_heads, pb.seq_len, pb.head_dim), dtype=torch.bfloat16, device=q.device)
     mmi_dense_prefill(pb, q, k, v, o, lse, stream)
     return o
+
+
+class HostSparsePrefill:
+    """End-to-end public call with HOST tensors: pinned host -> device copies of
+    the step's inputs, the four C-ABI calls, and a device -> host copy of the
+    output, all on one stream."""
+
+    def __init__(self, pb: Problem, cfgs: List[HeadConfig], device="cuda"):
+        self.sp = SparsePrefill(pb, cfgs, device)
+        H, Hkv, S, D = pb.n_heads, pb.n_kv_heads, pb.seq_len, pb.head_dim
+        self.q = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
+        self.k = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
+        self.v = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
+        self.lab = torch.empty((S,), dtype=torch.uint8, device=device)
+        self.o = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
+
+    def h2d_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.q, self.k, self.v, self.lab))
+
+    def d2h_bytes(self) -> int:
+        return self.o.numel() * self.o.element_size()
+
+    def __call__(self, q_h, k_h, v_h, lab_h, o_h, stream=None):
+        self.q.copy_(q_h, non_blocking=True)
+        self.k.copy_(k_h, non_blocking=True)
+        self.v.copy_(v_h, non_blocking=True)
+        self.lab.copy_(lab_h, non_blocking=True)
+        self.sp(self.q, self.k, self.v, self.lab, o=self.o, stream=stream)
+        o_h.copy_(self.o, non_blocking=True)
+        return o_h
