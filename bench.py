@@ -67,7 +67,7 @@ def count_launches(heads) -> int:
     n += 2 + 1 + 3                          # views (Q̄, K̄), inst params, items count / fill / gather
     n += 2                                  # permute gathers
     n += 1                                  # sparse attention
-    n += sum(1 for c in heads if any(p.kind == KIND_GRID and p.use_slash for p in _patterns(c)))  # merges
+    n += int(any(p.kind == KIND_GRID and p.use_slash for c in heads for p in _patterns(c)))  # LSE merge
     return n
 
 

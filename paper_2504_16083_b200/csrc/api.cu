@@ -152,6 +152,7 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
   CK(cudaMemsetAsync(at<char>(ws, P.bits), 0, P.bits.bytes, s));
   CK(cudaMemsetAsync(at<char>(ws, P.vs_cnt), 0, P.vs_cnt.bytes, s));
   CK(cudaMemsetAsync(at<char>(ws, P.seg_cnt), 0, P.seg_cnt.bytes, s));
+  CK(cudaMemsetAsync(at<char>(ws, P.grid_acc), 0, P.grid_acc.bytes, s));
   const int64_t mod_cap = (P.S + (int64_t)P.M * BLK + BLK - 1) / BLK * BLK;
   IndexCtx C = make_ctx(P, ws);
   int* info = at<int>(ws, P.mod_cnt);
@@ -167,7 +168,13 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
   int* srank = srows + ns * SLAB_ROWS;
   int* sinfo = srank + ns * SLAB_ROWS;
   const DSlab* dslabs = blob_at<DSlab>(ws, P, P.o_slabs);
-  launch_slabs(dslabs, (int)P.slabs.size(), q, k, S, P.H, P.Hkv, P.D, P.pb.last_q, tau_of(pb) * 1.4426950408889634f,
+  int max_batch = 1;
+  {
+    std::vector<int> per_kv(P.Hkv, 0);
+    for (const auto& sl : P.slabs) per_kv[sl.kv]++;
+    for (int c : per_kv) max_batch = std::max(max_batch, (c + 3) / 4);
+  }
+  launch_slabs(dslabs, (int)P.slabs.size(), max_batch, q, k, S, P.H, P.Hkv, P.D, P.pb.last_q, tau_of(pb) * 1.4426950408889634f,
                info, at<int>(ws, P.perm), at<int>(ws, P.rank), at<uint8_t>(ws, P.labels), srows, srank, sinfo,
                at<float2>(ws, P.slab_ml_part), at<float2>(ws, P.slab_ml), at<float>(ws, P.cbuf),
                at<unsigned long long>(ws, P.dgbuf), P.n_chunks, s);
@@ -175,7 +182,8 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
   const DInst* dinsts = blob_at<DInst>(ws, P, P.o_insts);
   launch_grid(dinsts, blob_at<int>(ws, P, P.o_gi), P.n_grid, P.max_ncand, (int)P.insts.size(), dslabs, sinfo, info,
               at<int>(ws, P.perm), at<float>(ws, P.cbuf), at<float>(ws, P.c_rank), S, P.S_pad,
-              at<GridRes>(ws, P.gridres), at<double>(ws, P.grid_part), s);
+              at<GridRes>(ws, P.gridres), at<double>(ws, P.grid_part), blob_at<int64_t>(ws, P, P.o_gacc),
+              at<unsigned long long>(ws, P.grid_acc), s);
   // a4 vertical-slash top-k
   launch_vs(dinsts, blob_at<int>(ws, P, P.o_vi), P.n_vs, dslabs, sinfo, info, at<int>(ws, P.perm),
             at<float>(ws, P.cbuf), at<unsigned long long>(ws, P.dgbuf), blob_at<int64_t>(ws, P, P.o_vsl),
@@ -285,12 +293,10 @@ extern "C" mmi_status mmi_unpermute(const mmi_problem* pb, const mmi_head_config
   cudaStream_t s = (cudaStream_t)stream;
   IndexCtx C = make_ctx(P, ws);
   const int64_t mod_cap = (P.S + (int64_t)P.M * BLK + BLK - 1) / BLK * BLK;
-  for (int h = 0; h < P.H; ++h) {
-    const DHead& hd = P.heads[h];
-    if (hd.part_rows0 < 0) continue;
-    const int rows = hd.qmod_view >= 0 ? (int)mod_cap : P.nb * BLK;
-    launch_merge(C, P.D, h, rows, o, lse, s);
-  }
+  // rows of the largest MAIN view among merged heads (rows beyond a head's view exit early)
+  int rows = 0;
+  for (int h : P.merge_heads) rows = std::max(rows, P.heads[h].qmod_view >= 0 ? (int)mod_cap : P.nb * BLK);
+  launch_merge(C, P.D, blob_at<int>(ws, P, P.o_mh), (int)P.merge_heads.size(), rows, o, lse, s);
   CK(cudaGetLastError());
   return MMI_OK;
 }

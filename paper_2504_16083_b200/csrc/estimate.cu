@@ -169,54 +169,55 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+constexpr int SLAB_BATCH = 4;  // slabs resident per CTA
+
 template <int D>
 struct SlabSmem {
-  static constexpr int LD = D + 8;
-  __nv_bfloat16 q[SLAB_ROWS * LD];
-  __nv_bfloat16 k[BLK * LD];
-  float a[SLAB_ROWS][BLK + 1];
-  int colidx[BLK];
-  int red[8];
+  static constexpr int LD = D + 8;  // padded rows: conflict-free ldmatrix
+  __nv_bfloat16 q[SLAB_BATCH][SLAB_ROWS * LD];
+  __nv_bfloat16 k[2][BLK * LD];     // cp.async double buffer
+  float a[2][SLAB_ROWS][BLK + 1];   // A-hat tiles of the two slabs in flight (pass 2)
+  int colidx[2][BLK];
+  int red[2][8];
+  int sl_idx[SLAB_BATCH];
+  int nsb;
 };
 
-// scores for one (slab, key tile): warp w holds rows 16w..16w+15, acc[nt][.] per mma layout
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// scores of one 16-row strip (rows of q_s) against one key tile: acc[nt][.] in mma layout
 template <int D>
-__device__ __forceinline__ void slab_tile_scores(const SlabSmem<D>& sm, float (&acc)[16][4]) {
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  constexpr int LD = SlabSmem<D>::LD;
+__device__ __forceinline__ void slab_strip_scores(const __nv_bfloat16* q_s, const __nv_bfloat16* k_s, int strip,
+                                                  float (&acc)[16][4]) {
+  const int lane = threadIdx.x % 32;
+  constexpr int LD = D + 8;
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 #pragma unroll
   for (int kk = 0; kk < D / 16; ++kk) {
     uint32_t a[4];
-    ldsm_x4(a, &sm.q[(warp * 16 + (lane % 16)) * LD + kk * 16 + (lane / 16) * 8]);
+    ldsm_x4(a, &q_s[(strip * 16 + (lane % 16)) * LD + kk * 16 + (lane / 16) * 8]);
 #pragma unroll
     for (int n2 = 0; n2 < 8; ++n2) {
       uint32_t b[4];
-      ldsm_x4(b, &sm.k[(n2 * 16 + (lane % 8) + (lane / 16) * 8) * LD + kk * 16 + ((lane / 8) % 2) * 8]);
+      ldsm_x4(b, &k_s[(n2 * 16 + (lane % 8) + (lane / 16) * 8) * LD + kk * 16 + ((lane / 8) % 2) * 8]);
       mma16816(acc[2 * n2], a, b[0], b[1]);
       mma16816(acc[2 * n2 + 1], a, b[2], b[3]);
     }
   }
 }
 
+// mode 0: pass 1 (row max / sum partials per key chunk); mode 1: pass 2 (A-hat -> c, dg)
+// grid (key chunk, KV group, slab batch); 8 warps: warps 0-3 / 4-7 take the two slabs of a pair.
 template <int D>
-__device__ __forceinline__ void load_rows_smem(__nv_bfloat16* dst, const __nv_bfloat16* src_base, const int* rows,
-                                               int nrows, int S, bool rows_are_list, int row0) {
-  constexpr int LD = D + 8;
-  constexpr int V = D / 8;  // uint4 per row
-  for (int i = threadIdx.x; i < nrows * V; i += blockDim.x) {
-    const int r = i / V, c = i % V;
-    const int pos = rows_are_list ? rows[r] : row0 + r;
-    uint4 val = make_uint4(0, 0, 0, 0);
-    if (pos >= 0 && pos < S) val = reinterpret_cast<const uint4*>(src_base + (size_t)pos * D)[c];
-    *reinterpret_cast<uint4*>(dst + r * LD + c * 8) = val;
-  }
-}
-
-// mode 0: pass 1 (row max / sum partials); mode 1: pass 2 (A-hat -> c, dg)
-template <int D>
-__global__ void __launch_bounds__(128) slab_kernel(int mode, const DSlab* __restrict__ slabs, int n_slabs,
+__global__ void __launch_bounds__(256) slab_kernel(int mode, const DSlab* __restrict__ slabs, int n_slabs,
                                                    const __nv_bfloat16* __restrict__ q,
                                                    const __nv_bfloat16* __restrict__ k, int S, int H,
                                                    float scale_log2, const int* __restrict__ rows,
@@ -227,157 +228,222 @@ __global__ void __launch_bounds__(128) slab_kernel(int mode, const DSlab* __rest
                                                    int n_chunks) {
   extern __shared__ __align__(16) uint8_t slab_smem_raw[];
   SlabSmem<D>& sm = *reinterpret_cast<SlabSmem<D>*>(slab_smem_raw);
-  const int chunk = blockIdx.x, kv = blockIdx.y;
+  constexpr int LD = SlabSmem<D>::LD;
+  const int chunk = blockIdx.x, kv = blockIdx.y, batch = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int g = lane / 4, t4 = lane % 4;
+  const int ps = warp / 4, strip = warp % 4;
   const int j_chunk0 = chunk * SLAB_CHUNK;
-  for (int si = 0; si < n_slabs; ++si) {
+  if (threadIdx.x == 0) {
+    int ord = 0, n = 0;
+    for (int si = 0; si < n_slabs; ++si) {
+      if (slabs[si].kv != kv) continue;
+      if (ord >= batch * SLAB_BATCH && ord < (batch + 1) * SLAB_BATCH) sm.sl_idx[n++] = si;
+      ++ord;
+    }
+    sm.nsb = n;
+  }
+  __syncthreads();
+  const int nsb = sm.nsb;
+  if (nsb == 0) return;
+  int maxpos = -1;
+  for (int b = 0; b < nsb; ++b) maxpos = max(maxpos, sinfo[sm.sl_idx[b] * 4 + 2]);
+  if (j_chunk0 > maxpos) {
+    if (mode == 0)
+      for (int b = 0; b < nsb; ++b)
+        if (threadIdx.x < SLAB_ROWS)
+          ml_part[((size_t)sm.sl_idx[b] * n_chunks + chunk) * SLAB_ROWS + threadIdx.x] = make_float2(-INFINITY, 0.f);
+    return;
+  }
+  // resident query slabs
+  constexpr int V = D / 8;
+  for (int b = 0; b < nsb; ++b) {
+    const int si = sm.sl_idx[b];
     const DSlab sl = slabs[si];
-    if (sl.kv != kv) continue;
-    const int L = sinfo[si * 4 + 0];
-    const int maxpos = sinfo[si * 4 + 2];
-    if (L == 0 || j_chunk0 > maxpos) {
-      if (mode == 0 && threadIdx.x < SLAB_ROWS)
-        ml_part[((size_t)si * n_chunks + chunk) * SLAB_ROWS + threadIdx.x] = make_float2(-INFINITY, 0.f);
-      continue;
+    for (int i = threadIdx.x; i < SLAB_ROWS * V; i += blockDim.x) {
+      const int r = i / V, c = i % V;
+      const int pos = rows[si * SLAB_ROWS + r];
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (pos >= 0) val = reinterpret_cast<const uint4*>(q + ((size_t)sl.head * S + pos) * D)[c];
+      *reinterpret_cast<uint4*>(&sm.q[b][r * LD + c * 8]) = val;
     }
-    const int* srow = rows + si * SLAB_ROWS;
+  }
+  const int ntile = min(SLAB_CHUNK / BLK, (maxpos - j_chunk0) / BLK + 1);
+  auto load_k = [&](int tt) {
+    const int j0 = j_chunk0 + tt * BLK;
+    __nv_bfloat16* dst = sm.k[tt & 1];
+    for (int i = threadIdx.x; i < BLK * V; i += blockDim.x) {
+      const int r = i / V, c = i % V;
+      const bool ok = j0 + r < S;
+      cp_async16(dst + r * LD + c * 8, k + ((size_t)kv * S + (ok ? j0 + r : 0)) * D + c * 8, ok);
+    }
+    cp_async_commit();
+  };
+  load_k(0);
+  // pass-1 running statistics: [pair][row lo / hi]
+  float m_run[2][2] = {{-INFINITY, -INFINITY}, {-INFINITY, -INFINITY}};
+  float l_run[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+  const int npair = (nsb + 1) / 2;
+  const double FX = 4503599627370496.0;  // 2^52
+  for (int tt = 0; tt < ntile; ++tt) {
+    if (tt + 1 < ntile) {
+      load_k(tt + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-    load_rows_smem<D>(sm.q, q + (size_t)sl.head * S * D, srow, SLAB_ROWS, S, true, 0);
-    const int r_lo = warp * 16 + g, r_hi = r_lo + 8;
-    const int pos_lo = srow[r_lo], pos_hi = srow[r_hi];
-    float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
-    float mr_lo = 0.f, mr_hi = 0.f, il_lo = 0.f, il_hi = 0.f;
-    if (mode == 1) {
-      const float2 a = ml[si * SLAB_ROWS + r_lo], b = ml[si * SLAB_ROWS + r_hi];
-      mr_lo = a.x;
-      il_lo = a.y > 0.f ? 1.f / a.y : 0.f;
-      mr_hi = b.x;
-      il_hi = b.y > 0.f ? 1.f / b.y : 0.f;
-    }
-    for (int tt = 0; tt < SLAB_CHUNK / BLK; ++tt) {
-      const int j0 = j_chunk0 + tt * BLK;
-      if (j0 > maxpos) break;
-      __syncthreads();
-      load_rows_smem<D>(sm.k, k + (size_t)kv * S * D, nullptr, BLK, S, false, j0);
-      __syncthreads();
+    const int j0 = j_chunk0 + tt * BLK;
+    const __nv_bfloat16* k_s = sm.k[tt & 1];
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      if (pp >= npair) break;
+      const int b = 2 * pp + ps;
+      const bool have = b < nsb;
+      const int si = have ? sm.sl_idx[b] : 0;
+      const int* srow = rows + si * SLAB_ROWS;
+      const int r_lo = strip * 16 + g, r_hi = r_lo + 8;
       float acc[16][4];
-      slab_tile_scores<D>(sm, acc);
-      // mask + scale
+      if (have) {
+        slab_strip_scores<D>(sm.q[b], k_s, strip, acc);
+        const int pos_lo = srow[r_lo], pos_hi = srow[r_hi];
 #pragma unroll
-      for (int nt = 0; nt < 16; ++nt) {
+        for (int nt = 0; nt < 16; ++nt) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = j0 + nt * 8 + 2 * t4 + (e & 1);
-          const int pr = (e < 2) ? pos_lo : pos_hi;
-          acc[nt][e] = (pr >= 0 && j <= pr) ? acc[nt][e] * scale_log2 : -INFINITY;
+          for (int e = 0; e < 4; ++e) {
+            const int j = j0 + nt * 8 + 2 * t4 + (e & 1);
+            const int pr = (e < 2) ? pos_lo : pos_hi;
+            acc[nt][e] = (pr >= 0 && j <= pr) ? acc[nt][e] * scale_log2 : -INFINITY;
+          }
         }
       }
       if (mode == 0) {
-        float tm_lo = -INFINITY, tm_hi = -INFINITY;
+        if (have) {
+          float tm_lo = -INFINITY, tm_hi = -INFINITY;
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt) {
-          tm_lo = fmaxf(tm_lo, fmaxf(acc[nt][0], acc[nt][1]));
-          tm_hi = fmaxf(tm_hi, fmaxf(acc[nt][2], acc[nt][3]));
-        }
-        tm_lo = fmaxf(tm_lo, __shfl_xor_sync(0xffffffffu, tm_lo, 1));
-        tm_lo = fmaxf(tm_lo, __shfl_xor_sync(0xffffffffu, tm_lo, 2));
-        tm_hi = fmaxf(tm_hi, __shfl_xor_sync(0xffffffffu, tm_hi, 1));
-        tm_hi = fmaxf(tm_hi, __shfl_xor_sync(0xffffffffu, tm_hi, 2));
-        const float nm_lo = fmaxf(m_lo, tm_lo), nm_hi = fmaxf(m_hi, tm_hi);
-        float s_lo = 0.f, s_hi = 0.f;
-        if (nm_lo > -INFINITY) {
+          for (int nt = 0; nt < 16; ++nt) {
+            tm_lo = fmaxf(tm_lo, fmaxf(acc[nt][0], acc[nt][1]));
+            tm_hi = fmaxf(tm_hi, fmaxf(acc[nt][2], acc[nt][3]));
+          }
+          tm_lo = fmaxf(tm_lo, __shfl_xor_sync(0xffffffffu, tm_lo, 1));
+          tm_lo = fmaxf(tm_lo, __shfl_xor_sync(0xffffffffu, tm_lo, 2));
+          tm_hi = fmaxf(tm_hi, __shfl_xor_sync(0xffffffffu, tm_hi, 1));
+          tm_hi = fmaxf(tm_hi, __shfl_xor_sync(0xffffffffu, tm_hi, 2));
+          const float nm_lo = fmaxf(m_run[pp][0], tm_lo), nm_hi = fmaxf(m_run[pp][1], tm_hi);
+          float s_lo = 0.f, s_hi = 0.f;
+          if (nm_lo > -INFINITY) {
 #pragma unroll
-          for (int nt = 0; nt < 16; ++nt) s_lo += exp2f(acc[nt][0] - nm_lo) + exp2f(acc[nt][1] - nm_lo);
-        }
-        if (nm_hi > -INFINITY) {
+            for (int nt = 0; nt < 16; ++nt) s_lo += exp2f(acc[nt][0] - nm_lo) + exp2f(acc[nt][1] - nm_lo);
+          }
+          if (nm_hi > -INFINITY) {
 #pragma unroll
-          for (int nt = 0; nt < 16; ++nt) s_hi += exp2f(acc[nt][2] - nm_hi) + exp2f(acc[nt][3] - nm_hi);
+            for (int nt = 0; nt < 16; ++nt) s_hi += exp2f(acc[nt][2] - nm_hi) + exp2f(acc[nt][3] - nm_hi);
+          }
+          s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 1);
+          s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 2);
+          s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 1);
+          s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 2);
+          l_run[pp][0] = (m_run[pp][0] > -INFINITY ? l_run[pp][0] * exp2f(m_run[pp][0] - nm_lo) : 0.f) + s_lo;
+          l_run[pp][1] = (m_run[pp][1] > -INFINITY ? l_run[pp][1] * exp2f(m_run[pp][1] - nm_hi) : 0.f) + s_hi;
+          m_run[pp][0] = nm_lo;
+          m_run[pp][1] = nm_hi;
         }
-        s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 1);
-        s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 2);
-        s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 1);
-        s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 2);
-        l_lo = (m_lo > -INFINITY ? l_lo * exp2f(m_lo - nm_lo) : 0.f) + s_lo;
-        l_hi = (m_hi > -INFINITY ? l_hi * exp2f(m_hi - nm_hi) : 0.f) + s_hi;
-        m_lo = nm_lo;
-        m_hi = nm_hi;
       } else {
-        // A-hat tile -> smem
+        // ---- pass 2: A-hat tile -> smem, then fixed-order column / diagonal sums ----
+        if (have) {
+          const float2 ma = ml[si * SLAB_ROWS + r_lo], mb = ml[si * SLAB_ROWS + r_hi];
+          const float il_lo = ma.y > 0.f ? 1.f / ma.y : 0.f, il_hi = mb.y > 0.f ? 1.f / mb.y : 0.f;
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt) {
-          const int c = nt * 8 + 2 * t4;
-          sm.a[r_lo][c] = acc[nt][0] > -INFINITY ? exp2f(acc[nt][0] - mr_lo) * il_lo : 0.f;
-          sm.a[r_lo][c + 1] = acc[nt][1] > -INFINITY ? exp2f(acc[nt][1] - mr_lo) * il_lo : 0.f;
-          sm.a[r_hi][c] = acc[nt][2] > -INFINITY ? exp2f(acc[nt][2] - mr_hi) * il_hi : 0.f;
-          sm.a[r_hi][c + 1] = acc[nt][3] > -INFINITY ? exp2f(acc[nt][3] - mr_hi) * il_hi : 0.f;
+          for (int nt = 0; nt < 16; ++nt) {
+            const int c = nt * 8 + 2 * t4;
+            sm.a[ps][r_lo][c] = acc[nt][0] > -INFINITY ? exp2f(acc[nt][0] - ma.x) * il_lo : 0.f;
+            sm.a[ps][r_lo][c + 1] = acc[nt][1] > -INFINITY ? exp2f(acc[nt][1] - ma.x) * il_lo : 0.f;
+            sm.a[ps][r_hi][c] = acc[nt][2] > -INFINITY ? exp2f(acc[nt][2] - mb.x) * il_hi : 0.f;
+            sm.a[ps][r_hi][c + 1] = acc[nt][3] > -INFINITY ? exp2f(acc[nt][3] - mb.x) * il_hi : 0.f;
+          }
         }
-        if (sl.rank_mode) {
-          // compact the keys of modality qmod in this tile (ranks are consecutive)
-          const int j = j0 + threadIdx.x;
-          const bool isa = (j < S) && labels[j] == sl.qmod;
-          const unsigned bal = __ballot_sync(0xffffffffu, isa);
-          if (lane == 0) sm.red[warp] = __popc(bal);
-          __syncthreads();
-          int base = 0;
-          for (int w = 0; w < warp; ++w) base += sm.red[w];
-          if (isa) sm.colidx[base + __popc(bal & ((1u << lane) - 1u))] = threadIdx.x;
-          if (threadIdx.x == 0) sm.red[4] = sm.red[0] + sm.red[1] + sm.red[2] + sm.red[3];
+        // rank-mode slabs: compact the keys of the slab's modality (ranks are consecutive)
+        const int tid = threadIdx.x % 128;  // thread within this slab's half
+        const DSlab sl = slabs[si];
+        bool isa = false;
+        unsigned bal = 0;
+        if (have && sl.rank_mode && sl.need_dg) {
+          const int j = j0 + tid;
+          isa = (j < S) && labels[j] == sl.qmod;
+          bal = __ballot_sync(0xffffffffu, isa);
+          if (lane == 0) sm.red[ps][strip] = __popc(bal);
         }
         __syncthreads();
-        // column mass: fixed order over rows
-        {
-          const int c = threadIdx.x;
-          const int j = j0 + c;
-          float sum = 0.f;
-          for (int r = 0; r < SLAB_ROWS; ++r) sum += sm.a[r][c];
-          if (j < S) cbuf[sl.c_off + j] = sum;
+        if (have && sl.rank_mode && sl.need_dg) {
+          int base = 0;
+          for (int w = 0; w < strip; ++w) base += sm.red[ps][w];
+          if (isa) sm.colidx[ps][base + __popc(bal & ((1u << lane) - 1u))] = tid;
         }
-        // diagonal mass -> fixed point
-        const double FX = 4503599627370496.0;  // 2^52
-        if (!sl.rank_mode) {
-          // contiguous runs of slab rows
-          int r0 = 0;
-          while (r0 < L) {
-            int r1 = r0 + 1;
-            while (r1 < L && srow[r1] == srow[r1 - 1] + 1) ++r1;
-            const int pb = srow[r0] - r0;  // pos_r = pb + r
-            const int width = 127 + (r1 - r0);
-            for (int i = threadIdx.x; i < width; i += blockDim.x) {
-              const int o = pb + r0 - (j0 + 127) + i;
-              if (o < 0) continue;
-              float sum = 0.f;
-              for (int r = r0; r < r1; ++r) {
-                const int c = pb + r - o - j0;
-                if (c >= 0 && c < BLK) sum += sm.a[r][c];
-              }
-              if (sum > 0.f) atomicAdd(dgbuf + sl.dg_off + o, (unsigned long long)((double)sum * FX));
-            }
-            r0 = r1;
+        __syncthreads();
+        if (have) {
+          const int L = sinfo[si * 4 + 0];
+          // column mass
+          {
+            const int j = j0 + tid;
+            float sum = 0.f;
+            for (int r = 0; r < SLAB_ROWS; ++r) sum += sm.a[ps][r][tid];
+            if (j < S) cbuf[sl.c_off + j] = sum;
           }
-        } else {
-          const int Ka = sm.red[4];
-          if (Ka > 0) {
-            const int rank_lo = rank[j0 + sm.colidx[0]];
-            const int rho0 = rranks[si * SLAB_ROWS];  // slab ranks are consecutive
-            const int width = L + Ka - 1;
-            for (int i = threadIdx.x; i < width; i += blockDim.x) {
-              const int o = rho0 - (rank_lo + Ka - 1) + i;
-              if (o < 0) continue;
-              float sum = 0.f;
-              for (int r = 0; r < L; ++r) {
-                const int kr = rho0 + r - o - rank_lo;
-                if (kr >= 0 && kr < Ka) sum += sm.a[r][sm.colidx[kr]];
+          if (!sl.need_dg) {
+            // no slash selection reads this slab's diagonal mass
+          } else if (!sl.rank_mode) {
+            int r0 = 0;
+            while (r0 < L) {
+              int r1 = r0 + 1;
+              while (r1 < L && srow[r1] == srow[r1 - 1] + 1) ++r1;
+              const int pb = srow[r0] - r0;
+              const int width = 127 + (r1 - r0);
+              for (int i = tid; i < width; i += 128) {
+                const int o = pb + r0 - (j0 + 127) + i;
+                if (o < 0) continue;
+                float sum = 0.f;
+                for (int r = r0; r < r1; ++r) {
+                  const int c = pb + r - o - j0;
+                  if (c >= 0 && c < BLK) sum += sm.a[ps][r][c];
+                }
+                if (sum > 0.f) atomicAdd(dgbuf + sl.dg_off + o, (unsigned long long)((double)sum * FX));
               }
-              if (sum > 0.f) atomicAdd(dgbuf + sl.dg_off + o, (unsigned long long)((double)sum * FX));
+              r0 = r1;
+            }
+          } else {
+            const int Ka = sm.red[ps][0] + sm.red[ps][1] + sm.red[ps][2] + sm.red[ps][3];
+            if (Ka > 0) {
+              const int rank_lo = rank[j0 + sm.colidx[ps][0]];
+              const int rho0 = rranks[si * SLAB_ROWS];
+              const int width = L + Ka - 1;
+              for (int i = tid; i < width; i += 128) {
+                const int o = rho0 - (rank_lo + Ka - 1) + i;
+                if (o < 0) continue;
+                float sum = 0.f;
+                for (int r = 0; r < L; ++r) {
+                  const int kr = rho0 + r - o - rank_lo;
+                  if (kr >= 0 && kr < Ka) sum += sm.a[ps][r][sm.colidx[ps][kr]];
+                }
+                if (sum > 0.f) atomicAdd(dgbuf + sl.dg_off + o, (unsigned long long)((double)sum * FX));
+              }
             }
           }
         }
+        __syncthreads();
       }
     }
-    if (mode == 0 && t4 == 0) {
-      ml_part[((size_t)si * n_chunks + chunk) * SLAB_ROWS + r_lo] = make_float2(m_lo, l_lo);
-      ml_part[((size_t)si * n_chunks + chunk) * SLAB_ROWS + r_hi] = make_float2(m_hi, l_hi);
+    __syncthreads();  // all warps done with this K buffer before it is refilled
+  }
+  if (mode == 0 && t4 == 0) {
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const int b = 2 * pp + ps;
+      if (pp < npair && b < nsb) {
+        const int si = sm.sl_idx[b];
+        const int r_lo = strip * 16 + g, r_hi = r_lo + 8;
+        ml_part[((size_t)si * n_chunks + chunk) * SLAB_ROWS + r_lo] = make_float2(m_run[pp][0], l_run[pp][0]);
+        ml_part[((size_t)si * n_chunks + chunk) * SLAB_ROWS + r_hi] = make_float2(m_run[pp][1], l_run[pp][1]);
+      }
     }
   }
 }
@@ -395,34 +461,35 @@ __global__ void slab_combine_kernel(const float2* __restrict__ ml_part, int n_ch
   ml[si * SLAB_ROWS + r] = make_float2(m, l);
 }
 
-void launch_slabs(const DSlab* slabs, int n_slabs, const void* q, const void* k, int S, int H, int Hkv, int D,
-                  int last_q, float scale_log2, const int* info, const int* perm, const int* rank,
+template <int D>
+static void launch_slab_passes(dim3 grid, const DSlab* slabs, int n_slabs, const void* q, const void* k, int S, int H,
+                               float scale_log2, int* rows, int* rranks, int* sinfo, const uint8_t* labels,
+                               const int* rank, float2* ml_part, float2* ml, float* cbuf, unsigned long long* dgbuf,
+                               int n_chunks, cudaStream_t st) {
+  const int smem = sizeof(SlabSmem<D>);
+  cudaFuncSetAttribute(slab_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  slab_kernel<D><<<grid, 256, smem, st>>>(0, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S, H,
+                                          scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf, dgbuf,
+                                          n_chunks);
+  slab_combine_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(ml_part, n_chunks, ml);
+  slab_kernel<D><<<grid, 256, smem, st>>>(1, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S, H,
+                                          scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf, dgbuf,
+                                          n_chunks);
+}
+
+void launch_slabs(const DSlab* slabs, int n_slabs, int max_batch, const void* q, const void* k, int S, int H, int Hkv,
+                  int D, int last_q, float scale_log2, const int* info, const int* perm, const int* rank,
                   const uint8_t* labels, int* rows, int* rranks, int* sinfo, float2* ml_part, float2* ml, float* cbuf,
                   unsigned long long* dgbuf, int n_chunks, cudaStream_t st) {
   if (n_slabs == 0) return;
   slab_rows_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(slabs, S, last_q, info, perm, rank, rows, rranks, sinfo);
-  dim3 grid(n_chunks, Hkv);
-  if (D == 128) {
-    const int smem = sizeof(SlabSmem<128>);
-    cudaFuncSetAttribute(slab_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    slab_kernel<128><<<grid, 128, smem, st>>>(0, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S,
-                                              H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf,
-                                              dgbuf, n_chunks);
-    slab_combine_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(ml_part, n_chunks, ml);
-    slab_kernel<128><<<grid, 128, smem, st>>>(1, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S,
-                                              H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf,
-                                              dgbuf, n_chunks);
-  } else {
-    const int smem = sizeof(SlabSmem<64>);
-    cudaFuncSetAttribute(slab_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    slab_kernel<64><<<grid, 128, smem, st>>>(0, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S,
-                                             H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf,
-                                             dgbuf, n_chunks);
-    slab_combine_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(ml_part, n_chunks, ml);
-    slab_kernel<64><<<grid, 128, smem, st>>>(1, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S,
-                                             H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf,
-                                             dgbuf, n_chunks);
-  }
+  dim3 grid(n_chunks, Hkv, max_batch);
+  if (D == 128)
+    launch_slab_passes<128>(grid, slabs, n_slabs, q, k, S, H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part,
+                            ml, cbuf, dgbuf, n_chunks, st);
+  else
+    launch_slab_passes<64>(grid, slabs, n_slabs, q, k, S, H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part,
+                           ml, cbuf, dgbuf, n_chunks, st);
 }
 
 // =============================================================== a3: grid
@@ -461,32 +528,77 @@ __device__ __forceinline__ void grid_window(const DInst& x, const int* sinfo, co
   hi = min(wmin - FOLD_GAP, n);
 }
 
-// T = sum_W c (fp64, fixed order)
-__global__ void grid_total_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst,
-                                  const DSlab* __restrict__ slabs, const int* __restrict__ sinfo,
-                                  const int* __restrict__ info, const float* __restrict__ cbuf,
-                                  const float* __restrict__ c_rank, int S, int S_pad, GridRes* __restrict__ res) {
-  const int gi = blockIdx.x;
+// Fold (reading C4-C6): m_s[p] = sum_{j in W, j = p mod s} c[j] for every candidate stride.
+// One CTA per (group of 32 strides, chunk of W): the chunk of c is converted once
+// to 2^-52 fixed point in shared memory, each stride is reduced thread-per-phase,
+// and the per-chunk sums are flushed with 64-bit integer atomics.  Integer
+// addition is associative, so the fold is exact and order-independent
+// (deterministic) for any schedule.
+constexpr int FOLD_CHUNK = 4096;
+constexpr int FOLD_SG = 32;  // strides per CTA
+constexpr double FX52 = 4503599627370496.0;
+
+__global__ void __launch_bounds__(256) grid_acc_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst,
+                                                       const DSlab* __restrict__ slabs, const int* __restrict__ sinfo,
+                                                       const int* __restrict__ info, const float* __restrict__ cbuf,
+                                                       const float* __restrict__ c_rank, int S, int S_pad,
+                                                       const int64_t* __restrict__ acc_off,
+                                                       unsigned long long* __restrict__ acc) {
+  __shared__ unsigned long long chunk[FOLD_CHUNK];  // c over this part of W, 2^-52 fixed point
+  __shared__ unsigned long long part[256];
+  const int gi = blockIdx.z;
   const DInst x = insts[grid_inst[gi]];
+  const int s0 = x.smin + blockIdx.x * FOLD_SG;
+  if (s0 > x.smax) return;
   int lo, hi, n;
   grid_window(x, sinfo, info, S, lo, hi, n);
+  const int j_begin = lo + blockIdx.y * FOLD_CHUNK;
+  const int j_end = min(hi, j_begin + FOLD_CHUNK);
+  if (j_begin >= j_end) return;
+  const int len = j_end - j_begin;
+  const int ns = min(FOLD_SG, x.smax - s0 + 1);
   const float* c = x.rank ? c_rank + (size_t)gi * S_pad : cbuf + slabs[x.slab].c_off;
-  double sum = 0.0;
-  for (int j = lo + threadIdx.x; j < hi; j += blockDim.x) sum += c[j];
-  typedef cub::BlockReduce<double, 256> R;
-  __shared__ typename R::TempStorage tmp;
-  const double T = R(tmp).Sum(sum);
-  if (threadIdx.x == 0) {
-    res[gi].T = T;
-    res[gi].valid = 0;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) chunk[i] = (unsigned long long)((double)c[j_begin + i] * FX52);
+  __syncthreads();
+  unsigned long long* g = acc + acc_off[gi];
+  const int tid = threadIdx.x;
+  for (int q = 0; q < ns; ++q) {
+    const int s = s0 + q;
+    unsigned long long* gs = g + (size_t)(s - x.smin) * x.smax;
+    if (s <= 256) {
+      const int G = 256 / s;
+      unsigned long long sum = 0;
+      if (tid < G * s) {
+        const int grp = tid / s, p = tid % s;
+        // first local index with (j_begin + i) = p (mod s)
+        const int i0 = (((p - j_begin) % s) + s) % s;
+        for (int i = i0 + grp * s; i < len; i += G * s) sum += chunk[i];
+      }
+      part[tid] = sum;
+      __syncthreads();
+      if (tid < s) {
+        unsigned long long tot = 0;
+        for (int grp = 0; grp < G; ++grp) tot += part[grp * s + tid];
+        if (tot) atomicAdd(&gs[tid], tot);
+      }
+      __syncthreads();
+    } else {
+      for (int p = tid; p < s; p += blockDim.x) {
+        const int i0 = (((p - j_begin) % s) + s) % s;
+        unsigned long long sum = 0;
+        for (int i = i0; i < len; i += s) sum += chunk[i];
+        if (sum) atomicAdd(&gs[p], sum);
+      }
+    }
   }
 }
 
-__global__ void __launch_bounds__(256) grid_fold_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst,
-                                                        const DSlab* __restrict__ slabs, const int* __restrict__ sinfo,
-                                                        const int* __restrict__ info, const float* __restrict__ cbuf,
-                                                        const float* __restrict__ c_rank, int S, int S_pad,
-                                                        const GridRes* __restrict__ res, double* __restrict__ part) {
+// J(s, p) = m_s[p] - n_s[p] * T / N for one candidate stride; best phase (ties -> smaller p)
+__global__ void __launch_bounds__(256) grid_eval_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst,
+                                                        const int* __restrict__ sinfo, const int* __restrict__ info, int S,
+                                                        const int64_t* __restrict__ acc_off,
+                                                        const unsigned long long* __restrict__ acc,
+                                                        double* __restrict__ part, GridRes* __restrict__ res) {
   const int gi = blockIdx.y;
   const DInst x = insts[grid_inst[gi]];
   const int s = x.smin + blockIdx.x;
@@ -495,6 +607,19 @@ __global__ void __launch_bounds__(256) grid_fold_kernel(const DInst* __restrict_
   int lo, hi, n;
   grid_window(x, sinfo, info, S, lo, hi, n);
   const int N = hi - lo;
+  const unsigned long long* g = acc + acc_off[gi];
+  // T = sum over all phases of the smallest candidate stride (= sum of c over W, exact)
+  typedef cub::BlockReduce<unsigned long long, 256> RU;
+  __shared__ typename RU::TempStorage tmpu;
+  unsigned long long tl = 0;
+  for (int p = threadIdx.x; p < x.smin; p += blockDim.x) tl += g[p];
+  const unsigned long long Tfx = RU(tmpu).Sum(tl);
+  __shared__ double T_s;
+  if (threadIdx.x == 0) {
+    T_s = (double)Tfx / FX52;
+    if (blockIdx.x == 0) res[gi].T = T_s;
+  }
+  __syncthreads();
   if (N < s || s < 1) {
     if (threadIdx.x == 0) {
       out[0] = -INFINITY;
@@ -502,45 +627,20 @@ __global__ void __launch_bounds__(256) grid_fold_kernel(const DInst* __restrict_
     }
     return;
   }
-  const float* c = x.rank ? c_rank + (size_t)gi * S_pad : cbuf + slabs[x.slab].c_off;
-  const double T = res[gi].T;
-  __shared__ double part_s[256];
+  const double T = T_s;
   typedef cub::BlockReduce<JP, 256> R;
   __shared__ typename R::TempStorage tmp;
   JP best;
   best.J = -INFINITY;
   best.p = INT_MAX;
-  if (s <= 256) {
-    const int G = 256 / s;
-    const int tid = threadIdx.x;
-    double acc = 0.0;
-    if (tid < G * s) {
-      const int grp = tid / s, p = tid % s;
-      const int j0 = lo + (((p - lo) % s) + s) % s;
-      for (int j = j0 + grp * s; j < hi; j += G * s) acc += c[j];
-    }
-    part_s[tid] = acc;
-    __syncthreads();
-    if (tid < s) {
-      double m = 0.0;
-      for (int grp = 0; grp < G; ++grp) m += part_s[grp * s + tid];
-      const int p = tid;
-      const int j0 = lo + (((p - lo) % s) + s) % s;
-      const int np = j0 < hi ? (hi - 1 - j0) / s + 1 : 0;
-      best.J = m - (double)np * T / (double)N;
-      best.p = p;
-    }
-  } else {
-    for (int p = threadIdx.x; p < s; p += 256) {
-      const int j0 = lo + (((p - lo) % s) + s) % s;
-      double m = 0.0;
-      for (int j = j0; j < hi; j += s) m += c[j];
-      const int np = j0 < hi ? (hi - 1 - j0) / s + 1 : 0;
-      JP cand;
-      cand.J = m - (double)np * T / (double)N;
-      cand.p = p;
-      best = jp_best(best, cand);
-    }
+  for (int p = threadIdx.x; p < s; p += blockDim.x) {
+    const double m = (double)g[(size_t)(s - x.smin) * x.smax + p] / FX52;
+    const int j0 = lo + (((p - lo) % s) + s) % s;
+    const int np = j0 < hi ? (hi - 1 - j0) / s + 1 : 0;
+    JP cand;
+    cand.J = m - (double)np * T / (double)N;
+    cand.p = p;
+    best = jp_best(best, cand);
   }
   const JP b = R(tmp).Reduce(best, JPMax());
   if (threadIdx.x == 0) {
@@ -549,39 +649,60 @@ __global__ void __launch_bounds__(256) grid_fold_kernel(const DInst* __restrict_
   }
 }
 
-__global__ void grid_pick_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst, int n_grid,
-                                 const double* __restrict__ part, GridRes* __restrict__ res) {
-  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gi >= n_grid) return;
+struct JS {
+  double J;
+  int s, p;
+};
+struct JSMax {
+  __device__ __forceinline__ JS operator()(const JS& a, const JS& b) const {
+    if (b.J > a.J || (b.J == a.J && b.s < a.s)) return b;
+    return a;
+  }
+};
+
+// argmax over strides: larger J, ties -> smaller stride
+__global__ void __launch_bounds__(1024) grid_pick_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst,
+                                                         const double* __restrict__ part, GridRes* __restrict__ res) {
+  const int gi = blockIdx.x;
   const DInst x = insts[grid_inst[gi]];
-  double bJ = -INFINITY;
-  int bs = x.smin, bp = 0, valid = 0;
-  for (int s = x.smin; s <= x.smax; ++s) {
+  JS best;
+  best.J = -INFINITY;
+  best.s = INT_MAX;
+  best.p = 0;
+  for (int s = x.smin + threadIdx.x; s <= x.smax; s += blockDim.x) {
     const double J = part[((size_t)gi * 1025 + (s - x.smin)) * 2];
     if (J == -INFINITY) continue;
-    if (!valid || J > bJ) {
-      bJ = J;
-      bs = s;
-      bp = (int)part[((size_t)gi * 1025 + (s - x.smin)) * 2 + 1];
-      valid = 1;
-    }
+    JS c;
+    c.J = J;
+    c.s = s;
+    c.p = (int)part[((size_t)gi * 1025 + (s - x.smin)) * 2 + 1];
+    best = JSMax()(best, c);
   }
-  res[gi].s = bs;
-  res[gi].p = valid ? bp : 0;
-  res[gi].J = valid ? bJ : 0.0;
-  res[gi].valid = valid;
+  typedef cub::BlockReduce<JS, 1024> R;
+  __shared__ typename R::TempStorage tmp;
+  const JS b = R(tmp).Reduce(best, JSMax());
+  if (threadIdx.x == 0) {
+    const bool valid = b.s != INT_MAX;
+    res[gi].s = valid ? b.s : x.smin;
+    res[gi].p = valid ? b.p : 0;
+    res[gi].J = valid ? b.J : 0.0;
+    res[gi].valid = valid;
+  }
 }
 
 void launch_grid(const DInst* insts, const int* grid_inst, int n_grid, int max_ncand, int n_inst_total,
                  const DSlab* slabs, const int* sinfo, const int* info, const int* perm, const float* cbuf,
-                 float* c_rank, int S, int S_pad, GridRes* res, double* part, cudaStream_t st) {
+                 float* c_rank, int S, int S_pad, GridRes* res, double* part, const int64_t* acc_off,
+                 unsigned long long* acc, cudaStream_t st) {
   if (n_grid == 0) return;
   grid_gather_rank_kernel<<<dim3(64, n_inst_total), 256, 0, st>>>(insts, n_inst_total, slabs, info, perm, cbuf,
                                                                    c_rank, S_pad);
-  grid_total_kernel<<<n_grid, 256, 0, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S, S_pad, res);
-  grid_fold_kernel<<<dim3(max_ncand, n_grid), 256, 0, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S,
-                                                            S_pad, res, part);
-  grid_pick_kernel<<<(n_grid + 63) / 64, 64, 0, st>>>(insts, grid_inst, n_grid, part, res);
+  const int n_sg = (max_ncand + FOLD_SG - 1) / FOLD_SG;
+  const int n_ch = (S + FOLD_CHUNK - 1) / FOLD_CHUNK;
+  grid_acc_kernel<<<dim3(n_sg, n_ch, n_grid), 256, 0, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S,
+                                                              S_pad, acc_off, acc);
+  grid_eval_kernel<<<dim3(max_ncand, n_grid), 256, 0, st>>>(insts, grid_inst, sinfo, info, S, acc_off, acc, part, res);
+  grid_pick_kernel<<<n_grid, 1024, 0, st>>>(insts, grid_inst, part, res);
 }
 
 // =============================================================== a4: VS top-k

@@ -675,11 +675,12 @@ __global__ void gather_rows_kernel(const int* __restrict__ src, int64_t rows, co
 }
 
 // ================================================================ merge (a8)
-__global__ void merge_kernel(IndexCtx C, int D, int h, int n_rows, __nv_bfloat16* __restrict__ o,
-                             float* __restrict__ lse) {
+__global__ void merge_kernel(IndexCtx C, int D, const int* __restrict__ heads_list, int n_rows,
+                             __nv_bfloat16* __restrict__ o, float* __restrict__ lse) {
   const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   if (warp_g >= n_rows) return;
+  const int h = heads_list[blockIdx.y];
   const DHead hd = C.heads[h];
   const int i = warp_g;
   int pos, grp;
@@ -758,10 +759,12 @@ void launch_gather(const int* src, int64_t rows, int D, const void* a, void* a_o
     gather_rows_kernel<64><<<grid, 256, 0, st>>>(src, rows, (const __nv_bfloat16*)a, (__nv_bfloat16*)a_out,
                                                  (const __nv_bfloat16*)b, (__nv_bfloat16*)b_out);
 }
-void launch_merge(const IndexCtx& C, int D, int h, int n_rows, void* o, float* lse, cudaStream_t st) {
-  if (n_rows <= 0) return;
+void launch_merge(const IndexCtx& C, int D, const int* heads_list, int n_heads, int n_rows, void* o, float* lse,
+                  cudaStream_t st) {
+  if (n_rows <= 0 || n_heads <= 0) return;
   const int threads = n_rows * 32;
-  merge_kernel<<<(threads + 255) / 256, 256, 0, st>>>(C, D, h, n_rows, (__nv_bfloat16*)o, lse);
+  merge_kernel<<<dim3((threads + 255) / 256, n_heads), 256, 0, st>>>(C, D, heads_list, n_rows, (__nv_bfloat16*)o,
+                                                                     lse);
 }
 
 }  // namespace mmi

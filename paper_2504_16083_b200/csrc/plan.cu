@@ -169,6 +169,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
           slab_of_group[grp] = (int)P.slabs.size() - 1;
         }
         x.slab = slab_of_group[grp];
+        if (p.kind == MMI_PAT_VSLASH && p.n_slash > 0) P.slabs[x.slab].need_dg = 1;
       }
       // base size of the class views: S (original coordinates) or S (upper bound of n_a, rank coordinates)
       const int64_t nbase = S;
@@ -339,6 +340,12 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
     }
     if (P.insts[i].vs_id >= 0) P.vs_inst[P.insts[i].vs_id] = i;
   }
+  P.gacc_off.assign(std::max(P.n_grid, 1), 0);
+  for (int g = 0; g < P.n_grid; ++g) {
+    const DInst& x = P.insts[P.grid_inst[g]];
+    P.gacc_off[g] = P.gacc_words;
+    P.gacc_words += (int64_t)(x.smax - x.smin + 1) * x.smax;
+  }
   P.vs_off_tab.assign((size_t)4 * std::max(P.n_vs, 1), 0);
   for (int i = 0; i < P.n_vs; ++i) {
     P.vs_off_tab[2 * i] = P.vs_v_off[i];
@@ -363,6 +370,10 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
     sub(P.o_vi, sizeof(int) * P.vs_inst.size());
     sub(P.o_vsl, sizeof(int64_t) * 2 * std::max(P.n_vs, 1));
     sub(P.o_vsb, sizeof(int64_t) * 2 * std::max(P.n_vs, 1));
+    sub(P.o_gacc, sizeof(int64_t) * P.gacc_off.size());
+    for (int h = 0; h < H; ++h)
+      if (P.heads[h].part_rows0 >= 0) P.merge_heads.push_back(h);
+    sub(P.o_mh, sizeof(int) * std::max<size_t>(P.merge_heads.size(), 1));
     P.blob_bytes = b;
   }
   reg(P.blob, P.blob_bytes);
@@ -381,6 +392,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
   reg(P.c_rank, sizeof(float) * std::max(P.n_grid, 1) * nS);
   reg(P.gridres, sizeof(GridRes) * std::max(P.n_grid, 1));
   reg(P.grid_part, sizeof(double) * 2 * std::max(P.n_grid, 1) * 1025);
+  reg(P.grid_acc, sizeof(unsigned long long) * std::max<int64_t>(P.gacc_words, 1));
   reg(P.vs_lists, sizeof(int) * std::max<int64_t>(P.vs_list_words, 1));
   reg(P.vs_cnt, sizeof(int) * 2 * std::max(P.n_vs, 1));
   reg(P.bits, sizeof(uint32_t) * std::max<int64_t>(P.bits_words, 1));
@@ -427,6 +439,8 @@ std::vector<uint8_t> make_blob(const Plan& P) {
   const size_t nv = (size_t)std::max(P.n_vs, 1);
   put(P.o_vsl, P.vs_off_tab.data(), sizeof(int64_t) * 2 * nv);
   put(P.o_vsb, P.vs_off_tab.data() + 2 * nv, sizeof(int64_t) * 2 * nv);
+  put(P.o_gacc, P.gacc_off.data(), sizeof(int64_t) * P.gacc_off.size());
+  put(P.o_mh, P.merge_heads.data(), sizeof(int) * P.merge_heads.size());
   return b;
 }
 

@@ -45,6 +45,7 @@ struct DView {
 };
 struct DSlab {
   int32_t head, kv, qmod, rank_mode;   // qmod: modality of the slab rows (-1: last rows overall)
+  int32_t need_dg, pad0, pad1, pad2;   // need_dg: a vertical-slash instance with slashes uses this slab
   int64_t c_off;                       // float offset of c[S]
   int64_t dg_off;                      // u64 offset of dg[S]
 };
@@ -93,11 +94,16 @@ struct Plan {
   size_t o_heads = 0, o_insts = 0, o_views = 0, o_slabs = 0, o_passes = 0, o_qv = 0, o_kv = 0, o_gi = 0, o_vi = 0,
          o_vsl = 0, o_vsb = 0, blob_bytes = 0;
   int max_ncand = 1;
+  std::vector<int64_t> gacc_off;       // per grid instance: u64 offset of its [ncand][smax] fold accumulators
+  int64_t gacc_words = 0;
+  size_t o_gacc = 0;
+  std::vector<int> merge_heads;        // heads with partial rows (LSE merge in mmi_unpermute)
+  size_t o_mh = 0;
   // workspace regions
   Region blob;
   Region labels, mod_cnt, mod_off, perm, rank, modpos, modrank;
   Region slab_rows, slab_ml_part, slab_ml, cbuf, dgbuf, c_rank;
-  Region gridres, grid_part, vs_lists, vs_cnt, bits;
+  Region gridres, grid_part, grid_acc, vs_lists, vs_cnt, bits;
   Region view_len;
   Region qg_pos, qg_rank, qg_src, kg_pos, kg_rank, kg_src, qg, kg, vg;
   Region items, item_keys, item_vals, items_sorted, seg_cnt, seg_off, segs, inst_params, sort_tmp, scan_tmp;
