@@ -71,18 +71,7 @@ def count_launches(heads) -> int:
     return n
 
 
-def shard(H, Hkv, N, r):
-    """Heads [h0, h1) and KV heads [kv0, kv1) of rank r (KV-head-group sharding)."""
-    G = H // Hkv
-    if N <= Hkv:
-        g0, g1 = r * Hkv // N, (r + 1) * Hkv // N
-        return g0 * G, g1 * G, g0, g1
-    g = r * Hkv // N
-    ranks = [x for x in range(N) if x * Hkv // N == g]
-    i = ranks.index(r)
-    h0 = g * G + i * G // len(ranks)
-    h1 = g * G + (i + 1) * G // len(ranks)
-    return h0, h1, g, g + 1
+from paper_2504_16083_b200.dist import shard_heads as shard, all_ranges, exchange_output  # noqa: E402
 
 
 class ClockSampler:
@@ -220,13 +209,11 @@ def main():
     O = torch.empty((pb.n_heads, pb.seq_len, pb.head_dim), dtype=torch.bfloat16, device=dev)
     o = O[h0:h1]
     sp = mmi.SparsePrefill(lpb, lheads, device=dev)
-    ranges = [shard(pb.n_heads, pb.n_kv_heads, N, r) for r in range(N)]
+    ranges = all_ranges(pb.n_heads, pb.n_kv_heads, N)
 
     def gather_out():
         if N > 1:
-            works = [dist.broadcast(O[r0:r1], src=r, async_op=True) for r, (r0, r1, _, _) in enumerate(ranges)]
-            for w in works:
-                w.wait()
+            exchange_output(O, ranges, dist)
 
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731

@@ -1,0 +1,96 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol that
+include/mmi.h declares, sizes workspaces, and rejects invalid problems / configs
+on the host with the documented status codes (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from synth.config import HeadConfig, Problem, grid, ashape, vslash, none, full
+from synth.workloads import build_workload
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lib():
+    from paper_2504_16083_b200 import lib
+    return lib()
+
+
+def test_library_exports_header_symbols():
+    hdr = open(os.path.join(ROOT, "include", "mmi.h")).read()
+    names = re.findall(r"MMI_API\s+[\w\s\*]*?\b(mmi_\w+)\s*\(", hdr)
+    assert len(names) >= 10
+    L = _lib()
+    for n in names:
+        assert hasattr(L, n), n
+    assert L.mmi_version().startswith(b"mmi-b200")
+
+
+@pytest.mark.parametrize("idx", range(5))
+def test_workspace_sizes_for_baseline_configs(idx):
+    from paper_2504_16083_b200 import mmi_workspace_bytes
+    wl = build_workload(idx)
+    n = mmi_workspace_bytes(wl.problem, wl.heads)
+    assert n > 0
+    assert n < 64 << 30   # fits a 180 GB B200 with room for Q/K/V/O
+
+
+def _ws(pb, heads):
+    from paper_2504_16083_b200 import mmi_workspace_bytes
+    return mmi_workspace_bytes(pb, heads)
+
+
+def test_invalid_configs_rejected_on_host():
+    from paper_2504_16083_b200.mmi import lib, to_c_problem, to_c_configs
+    pb = Problem(2, 1, 4096, 128, n_modalities=2)
+    bad = [
+        [HeadConfig.no_boundary(none())] * 2,                                   # no keys for any row
+        [HeadConfig.no_boundary(ashape(128, 0))] * 2,                           # local < 1
+        [HeadConfig.no_boundary(vslash(0, 10))] * 2,                            # n_vertical < 1
+        [HeadConfig.no_boundary(grid(2000))] * 2,                               # stride > 1024
+        [HeadConfig.two_d([[grid(256), grid(256)], [ashape(), full()]])] * 2,   # grid on a cross pair
+        [HeadConfig.two_d([[none(), none()], [none(), full()]])] * 2,           # pair[a][a] NONE
+        [HeadConfig.two_d([[full(), vslash(10, 5)], [none(), full()]])] * 2,    # cross VS with slashes
+        [HeadConfig.q_boundary([grid(256), none()])] * 2,                       # Q-boundary modality NONE
+    ]
+    for heads in bad:
+        assert _ws(pb, heads) == 0
+        assert len(lib().mmi_last_error()) > 0
+    # shape errors
+    assert _ws(Problem(3, 2, 4096, 128), [HeadConfig.no_boundary(full())] * 3) == 0
+    assert b"multiple" in lib().mmi_last_error()
+    assert _ws(Problem(2, 1, 4096, 96), [HeadConfig.no_boundary(full())] * 2) == 0
+    assert _ws(Problem(2, 1, 0, 128), [HeadConfig.no_boundary(full())] * 2) == 0
+    # valid
+    assert _ws(pb, [HeadConfig.no_boundary(full())] * 2) > 0
+
+
+def test_compute_calls_validate_before_launch():
+    """Null workspace / pointers return a status (no launch, safe without a GPU)."""
+    from paper_2504_16083_b200.mmi import lib, to_c_problem, to_c_configs
+    pb = Problem(1, 1, 1024, 64)
+    heads = [HeadConfig.no_boundary(full())]
+    L = lib()
+    st = L.mmi_estimate_index(ctypes.byref(to_c_problem(pb)), to_c_configs(heads), None, None, None, None, 0, None)
+    assert st == 5  # MMI_E_WORKSPACE
+    st = L.mmi_dense_prefill(ctypes.byref(to_c_problem(pb)), None, None, None, None, None, None)
+    assert st == 1  # MMI_E_INVALID
+
+
+def test_binding_refuses_cpu_fallback():
+    """The product path never computes on the CPU: without CUDA the binding raises."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2504_16083_b200 import SparsePrefill
+    wl = build_workload(0)
+    sp_err = None
+    try:
+        sp = SparsePrefill(wl.problem, wl.heads, device="cpu")
+        q = torch.zeros(1, wl.problem.seq_len, 64, dtype=torch.bfloat16)
+        sp(q, q[:1], q[:1], torch.zeros(wl.problem.seq_len, dtype=torch.uint8))
+    except (RuntimeError, ValueError) as e:
+        sp_err = e
+    assert sp_err is not None
