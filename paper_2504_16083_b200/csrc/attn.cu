@@ -122,6 +122,26 @@ __device__ __forceinline__ void range_mask(uint32_t (&mw)[4], int lo, int hi) {
   }
 }
 
+// number of entries <= v in an ascending int array of 128 (shared memory)
+__device__ __forceinline__ int count_le(const int* a, int v) {
+  int i = 0;
+#pragma unroll
+  for (int step = 64; step > 0; step >>= 1)
+    if (a[i + step - 1] <= v) i += step;
+  return i + ((i == BLK - 1 && a[BLK - 1] <= v) ? 1 : 0);
+}
+
+// 128 bits of a bitmap starting at bit `lo` (bits below 0 read as 0): out[w] bit i = bit(lo + 32w + i)
+__device__ __forceinline__ void bit_window(const uint32_t* bits, int lo, uint32_t (&out)[4]) {
+  const int wb = (lo >= 0) ? (lo >> 5) : -((-lo + 31) >> 5);
+  const int sh = lo - wb * 32;
+  uint32_t w[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) w[i] = (wb + i >= 0) ? __ldg(bits + wb + i) : 0u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) out[i] = __funnelshift_r(w[i], w[i + 1], sh);
+}
+
 struct TileInfo {
   int krow;
   uint32_t space, pred, role, rmode, inst;
@@ -440,39 +460,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int kbase = e.krow - kv * P.S;
             if (!pred) {
               range_mask(mw, 0, BLK - 1);
-            } else if (!space) {
-              // original K: contiguous positions kbase + c, coordinates == positions
-              const int hi = xpos - kbase;  // causal: c <= hi
-              int sink = 0, local = 0;
-              if (!P.dense && role != R_TRUE) {
-                const InstParam ip = P.insts[it.inst_base + inst];
-                sink = ip.sink;
-                local = ip.local;
-              }
-              if (role == R_TRUE) {
-                range_mask(mw, 0, hi);
-              } else if (role == R_A) {
-                range_mask(mw, 0, min(hi, sink - 1 - kbase));
-                range_mask(mw, max(0, xpos - local + 1 - kbase), hi);
-              } else if (role == R_NOTA) {
-                range_mask(mw, max(0, sink - kbase), min(hi, xpos - local - kbase));
-              } else {
-                const InstParam ip = P.insts[it.inst_base + inst];
-                const uint32_t* sl_bits = P.bits + ip.slash_word;
-                const uint32_t* vm_bits = P.bits + ip.vmask_word;
-                const int x = rmode ? xrank : xpos;
-                for (int c = 0; c <= min(hi, BLK - 1); ++c) {
-                  const int y = kbase + c, o = x - y;
-                  const bool ok = ((sl_bits[o >> 5] >> (o & 31)) & 1u) && !((vm_bits[y >> 5] >> (y & 31)) & 1u);
-                  mw[c >> 5] |= (uint32_t)ok << (c & 31);
-                }
-              }
             } else {
-              // gathered K view: per-key positions / ranks from the stage
               int sink = 0, local = 0;
               const uint32_t* sl_bits = nullptr;
               const uint32_t* vm_bits = nullptr;
-              if (!P.dense) {
+              if (!P.dense && role != R_TRUE) {
                 const InstParam ip = P.insts[it.inst_base + inst];
                 sink = ip.sink;
                 local = ip.local;
@@ -480,22 +472,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (ip.vmask_word >= 0) vm_bits = P.bits + ip.vmask_word;
               }
               const int x = rmode ? xrank : xpos;
-              const int* kp = kpos_s + stage * BLK;
-              const int* kr = krank_s + stage * BLK;
-#pragma unroll 4
-              for (int c = 0; c < BLK; ++c) {
-                const int ypos = kp[c];
-                const int y = rmode ? kr[c] : ypos;
-                bool ok = ypos <= xpos;
-                if (role == R_A)
-                  ok = ok && ((y < sink) || (x - y < local));
-                else if (role == R_NOTA)
-                  ok = ok && (y >= sink) && (x - y >= local);
-                else if (role == R_VSSL && ok) {
-                  const int o = x - y;
-                  ok = ((sl_bits[o >> 5] >> (o & 31)) & 1u) && !((vm_bits[y >> 5] >> (y & 31)) & 1u);
-                }
-                mw[c >> 5] |= (uint32_t)ok << (c & 31);
+              // Keys of every view are ascending inside a tile, so each role is at most two
+              // index ranges: [0, n_causal) intersected with the pattern's coordinate ranges.
+              int n_causal, n_sink, n_lt_local, ybase;
+              if (!space) {
+                n_causal = min(max(xpos - kbase + 1, 0), BLK);
+                n_sink = min(max(sink - kbase, 0), BLK);
+                n_lt_local = min(max(x - local - kbase + 1, 0), BLK);  // keys with y <= x - local
+                ybase = kbase;
+              } else {
+                const int* kp = kpos_s + stage * BLK;
+                const int* yc = rmode ? (krank_s + stage * BLK) : kp;
+                n_causal = count_le(kp, xpos);
+                n_sink = (role == R_A || role == R_NOTA) ? count_le(yc, sink - 1) : 0;
+                n_lt_local = (role == R_A || role == R_NOTA) ? count_le(yc, x - local) : 0;
+                ybase = yc[0];
+              }
+              if (role == R_TRUE) {
+                range_mask(mw, 0, n_causal - 1);
+              } else if (role == R_A) {
+                range_mask(mw, 0, min(n_sink, n_causal) - 1);
+                range_mask(mw, n_lt_local, n_causal - 1);
+              } else if (role == R_NOTA) {
+                range_mask(mw, n_sink, min(n_lt_local, n_causal) - 1);
+              } else {
+                // vertical-slash: coordinates contiguous in the tile (original K, or a modality's
+                // rank-ordered keys); slash bits of offsets x - ybase - c, bit-reversed window
+                range_mask(mw, 0, n_causal - 1);
+                uint32_t ws[4], wv[4];
+                bit_window(sl_bits, x - ybase - (BLK - 1), ws);
+                bit_window(vm_bits, ybase, wv);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) mw[w] &= __brev(ws[3 - w]) & ~wv[w];
               }
             }
             if (P.fingerprint) {

@@ -297,7 +297,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
   P.seg_cap = segcap + 16;
 
   // VS lists / bitmaps
-  const int64_t bitw = (int64_t)S / 32 + 2;
+  const int64_t bitw = (int64_t)S / 32 + 8;  // slack: 128-bit windows may read past S
   for (int i = 0; i < P.n_vs; ++i) {
     P.vs_v_off.push_back(P.vs_list_words);
     P.vs_list_words += pad128(P.vs_nv[i]);

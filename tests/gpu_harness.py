@@ -123,8 +123,8 @@ def run_gpu(wl, d, want_fp: bool = True):
         fpt = torch.zeros((pb.n_heads, pb.seq_len, 3), dtype=torch.int64, device="cuda")
         mmi_sparse_fingerprint(pb, wl.heads, sp.ws, q, k, v, fpt)
         torch.cuda.synchronize()
-        fp = fpt.cpu().numpy()
-    return dict(o=o.float().cpu().numpy(), lse=lse.cpu().numpy(), exp=exps, fp=fp)
+        fp = fpt
+    return dict(o=o, lse=lse, exp=exps, fp=fp)   # device tensors: rows are pulled on demand
 
 
 def check_head(wl, d, gpu, h: int, rows: Optional[np.ndarray] = None, check_index=True) -> Dict:
@@ -141,13 +141,15 @@ def check_head(wl, d, gpu, h: int, rows: Optional[np.ndarray] = None, check_inde
     gidx = gpu_index_as_oracle(cfg, gpu["exp"][h], pb.n_modalities)
     r = run_head(pb, cfg, qh, kg, vg, d["labels"], rows=rows, index=gidx)
     rr = r["rows"]
-    err = np.abs(gpu["o"][h][rr] - r["O"])
+    ridx = torch.from_numpy(rr).to(gpu["o"].device)
+    og = gpu["o"][h].index_select(0, ridx).float().cpu().numpy()
+    err = np.abs(og - r["O"])
     out["max_err"] = float(err.max())
     out["mean_err"] = float(err.mean())
-    lse_g = gpu["lse"][h][rr]
+    lse_g = gpu["lse"][h].index_select(0, ridx).cpu().numpy()
     out["lse_err"] = float(np.abs(lse_g - r["lse"]).max())
     if gpu["fp"] is not None:
-        f = gpu["fp"][h][rr]
+        f = gpu["fp"][h].index_select(0, ridx).cpu().numpy()
         out["fp_count_ok"] = bool((f[:, 0] == r["count"]).all())
         out["fp_sum_ok"] = bool((f[:, 1].astype(np.uint64) == r["sumj"]).all())
         out["fp_sum2_ok"] = bool((f[:, 2].astype(np.uint64) == r["sumj2"]).all())
