@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tmem_ld32(tS[sbuf] + lane_off + c * 32, r);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(r[j]) * P.scale_log2;
+          for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(r[j]);  // raw scores
         }
         if (pred || (P.fingerprint && space)) mbar_wait(k_full + stage, kv_phase);
         if (pred || P.fingerprint) {
@@ -535,6 +535,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         float mt = -INFINITY;
 #pragma unroll
         for (int c = 0; c < BLK; ++c) mt = fmaxf(mt, s[c]);
+        if (mt > -INFINITY) mt *= P.scale_log2;  // tau * log2(e) > 0 commutes with max
         float alpha = 1.f;
         bool rescale = false;
         if (mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt > -INFINITY)) {
@@ -547,8 +548,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint32_t pk[BLK / 2];
 #pragma unroll
         for (int c = 0; c < BLK; c += 2) {
-          const float p0 = ex2(s[c] - mu);
-          const float p1 = ex2(s[c + 1] - mu);
+          const float p0 = ex2(fmaf(s[c], P.scale_log2, -mu));
+          const float p1 = ex2(fmaf(s[c + 1], P.scale_log2, -mu));
           ls += p0 + p1;
           pk[c / 2] = pack_bf16(p0, p1);
         }
