@@ -266,8 +266,15 @@ def main():
     sparse_ms = stage["sparse"]
     achieved = tiles * flops_tile / (sparse_ms * 1e-3) / 1e12
     peak = float(peaks["bf16_tflops"])
+    traffic = None
+    try:  # dram bytes per launch of this kernel, from the committed `ncu --set full` capture of this workload
+        tr = json.load(open(os.path.join(ROOT, "profiles", "attn_traffic.json")))
+        if tr.get("workload") == wl.name and N == 1:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "mmi::attn_kernel<%d>" % pb.head_dim, "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"
+            "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)", "kernel": "mmi::attn_kernel<%d>" % pb.head_dim, "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"
             if "_fallback" not in peaks else "fallback 1.59 PF", "tiles": int(tiles),
             "flops_per_tile": flops_tile}
 
