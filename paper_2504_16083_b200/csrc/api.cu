@@ -402,7 +402,7 @@ extern "C" mmi_status mmi_export_index(const mmi_problem* pb, const mmi_head_con
   for (const auto& it : items)
     if (it.head == head && it.n_tiles > 0) {
       ++n_it;
-      tiles += it.n_tiles;
+      tiles += (long long)it.n_tiles * (1 + it.has_b);  // computed 128x128 tiles (both halves)
       n_seg += it.n_segs;
     }
   out.push_back(n_it);

@@ -32,31 +32,43 @@
 
 namespace mmi {
 
-constexpr int NTHREADS = 256;
 constexpr float RESCALE_THRESH = 8.0f;  // lazy rescale: P <= 2^8 (log2 domain)
 
+// Work items cover two 128-row query blocks (halves A and B); each half has its
+// own softmax warpgroup, TMEM S/P buffer (128 columns) and O accumulator (128
+// columns): 512 columns total.  K/V tiles are shared by both halves.
 template <int D>
 struct Cfg {
-  static constexpr int KST = (D == 128) ? 3 : 4;  // K ring stages
+  static constexpr int KST = (D == 128) ? 2 : 3;  // K ring stages
   static constexpr int VST = (D == 128) ? 2 : 3;  // V ring stages
 };
 constexpr int SCHED_RING = 4;
+constexpr int NWARP_CTRL = 4;                     // scheduler+Q, MMA, K loader, V loader
+constexpr int NTHREADS = 32 * (NWARP_CTRL + 8);  // + two softmax warpgroups
+constexpr int LAUNCH_REGS = 168;                  // ptxas allocation at __launch_bounds__(384, 1)
+#ifndef MMI_CTRL_REGS
+#define MMI_CTRL_REGS 56
+#define MMI_SOFT_REGS 224
+#endif
+constexpr int CTRL_REGS = MMI_CTRL_REGS;                    // setmaxnreg budgets: .inc only draws on what .dec released
+constexpr int SOFT_REGS = MMI_SOFT_REGS;                    // inside the CTA's launch allocation (384*168), else it blocks forever
+static_assert(128 * CTRL_REGS + 256 * SOFT_REGS <= NTHREADS * LAUNCH_REGS, "setmaxnreg budget exceeds launch allocation");
 
 template <int D>
 struct Smem {
   static constexpr int KST = Cfg<D>::KST, VST = Cfg<D>::VST;
-  static constexpr int Q_BYTES = BLK * D * 2;
+  static constexpr int Q_BYTES = BLK * D * 2;  // one 128-row half
   static constexpr int KV_BYTES = BLK * D * 2;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
   static constexpr int OFF_KPOS = OFF_V + VST * KV_BYTES;
   static constexpr int OFF_KRANK = OFF_KPOS + KST * BLK * 4;
   static constexpr int OFF_SCHED = OFF_KRANK + KST * BLK * 4;
   static constexpr int OFF_BAR = OFF_SCHED + 64;
-  // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2] p_full[2]
-  // pv_done o_full o_empty sched_full[R] sched_empty[R]
-  static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 4 + 3 + 2 * SCHED_RING;
+  // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2] p_full[2] o_full[2] o_empty[2]
+  // sched_full[R] sched_empty[R]
+  static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 8 + 2 * SCHED_RING;
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
   static constexpr int TOTAL = OFF_TMEM + 16;
   static constexpr int ALLOC = TOTAL + 1024;  // alignment slack
@@ -64,20 +76,22 @@ struct Smem {
 
 struct ItemView {
   int head, q_row0, seg_off, n_segs, n_tiles, q_gathered, out_mode, out_row0, inst_base, skip_s, skip_p, skip_rank,
-      row_mod, rb;
+      row_mod, rb, has_b;
 };
 
 __device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx) {
   ItemView v;
   if (P.dense) {
     const int nb = (P.S + BLK - 1) / BLK;
-    const int rb = nb - 1 - idx / P.H;  // longest rows first (LPT)
+    const int npair = (nb + 1) / 2;
+    const int pk = npair - 1 - idx / P.H;  // longest rows first (LPT)
     v.head = idx % P.H;
-    v.q_row0 = v.head * P.S + rb * BLK;
-    v.rb = rb;
+    v.q_row0 = v.head * P.S + 2 * pk * BLK;
+    v.has_b = (2 * pk + 1 < nb) ? 1 : 0;
+    v.rb = 2 * pk + v.has_b;  // last row block of the pair
     v.seg_off = 0;
     v.n_segs = 1;
-    v.n_tiles = rb + 1;
+    v.n_tiles = v.rb + 1;
     v.q_gathered = 0;
     v.out_mode = OUT_FINAL;
     v.out_row0 = 0;
@@ -102,6 +116,7 @@ __device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx) {
   v.skip_p = w.skip_p;
   v.skip_rank = w.skip_rank;
   v.row_mod = w.row_mod;
+  v.has_b = w.has_b;
   v.rb = 0;
   return v;
 }
@@ -159,7 +174,7 @@ struct SegIter {
       cur.ntiles = it.rb + 1;
       cur.meta = seg_meta(0, R_TRUE, 0, 0);
       cur.pred_head = 0;
-      cur.pred_tail = 1;
+      cur.pred_tail = it.has_b ? 2 : 1;  // diagonal tiles of both halves
     } else {
       cur.ntiles = 0;
       seg_i = -1;
@@ -200,12 +215,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* k_empty = k_full + KST;
   uint64_t* v_full = k_empty + KST;
   uint64_t* v_empty = v_full + VST;
-  uint64_t* s_full = v_empty + VST;   // [2] S buffer written by the MMA
-  uint64_t* p_full = s_full + 2;      // [2] P (bf16, aliasing S in TMEM) written by the softmax
-  uint64_t* pv_done = p_full + 2;     // one phase per P V MMA
-  uint64_t* o_full = pv_done + 1;
-  uint64_t* o_empty = o_full + 1;
-  uint64_t* sched_full = o_empty + 1;
+  uint64_t* s_full = v_empty + VST;  // [2] per half: S written by the MMA
+  uint64_t* p_full = s_full + 2;     // [2] per half: P (bf16, aliasing S in TMEM) written by the softmax
+  uint64_t* o_full = p_full + 2;     // [2] per half
+  uint64_t* o_empty = o_full + 2;    // [2] per half
+  uint64_t* sched_full = o_empty + 2;
   uint64_t* sched_empty = sched_full + SCHED_RING;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
   int32_t* kpos_s = reinterpret_cast<int32_t*>(smem + L::OFF_KPOS);
@@ -220,7 +234,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_init(q_empty, 1);
     for (int i = 0; i < KST; ++i) {
       mbar_init(k_full + i, 1);
-      mbar_init(k_empty + i, 1 + 4);  // S-MMA commit + one arrival per softmax warp (key coords consumed)
+      mbar_init(k_empty + i, 1 + 8);  // last S-MMA commit + one arrival per softmax warp (key coords consumed)
     }
     for (int i = 0; i < VST; ++i) {
       mbar_init(v_full + i, 1);
@@ -229,13 +243,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 128);
+      mbar_init(o_full + i, 1);
+      mbar_init(o_empty + i, 128);
     }
-    mbar_init(pv_done, 1);
-    mbar_init(o_full, 1);
-    mbar_init(o_empty, 128);
     for (int i = 0; i < SCHED_RING; ++i) {
       mbar_init(sched_full + i, 1);
-      mbar_init(sched_empty + i, 3 + 4);  // K loader, V loader, MMA, 4 softmax warps
+      mbar_init(sched_empty + i, 3 + 8);  // K loader, V loader, MMA, 8 softmax warps
     }
     fence_barrier_init();
   }
@@ -252,160 +265,181 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  const uint32_t tS[2] = {tmem, tmem + 128};
-  const uint32_t tO = tmem + 256;
-
-  const int n_items = P.dense ? P.H * ((P.S + BLK - 1) / BLK) : P.n_items;
-  // consumer side of the work-item ring
+  // TMEM columns: S/P of half h at 128 h, O of half h at 256 + 128 h
+  const int n_items = P.dense ? P.H * ((((P.S + BLK - 1) / BLK) + 1) / 2) : P.n_items;
   auto fetch = [&](int i) -> int {
     const int slot = i % SCHED_RING;
     mbar_wait(sched_full + slot, (i / SCHED_RING) & 1);
     return sched_ring[slot];
   };
 
-  if (warp == 0) {
-    // ======================= scheduler + Q loader =======================
-    if (elect_one()) {
-      uint32_t q_phase = 0;
-      for (int i = 0;; ++i) {
-        const int slot = i % SCHED_RING;
-        mbar_wait(sched_empty + slot, ((i / SCHED_RING) & 1) ^ 1);
-        int idx = (i == 0) ? (int)blockIdx.x : (int)gridDim.x + (int)atomicAdd(P.sched, 1u);
-        if (idx >= n_items) idx = -1;
-        sched_ring[slot] = idx;
-        mbar_arrive(sched_full + slot);
-        if (idx < 0) break;
-        const ItemView it = load_item(P, idx);
-        if (it.n_tiles <= 0) continue;
-        if (P.dbg) P.dbg[idx * 8 + 0] = gtimer();
-        mbar_wait(q_empty, q_phase ^ 1);
-        if (P.dbg) P.dbg[idx * 8 + 1] = gtimer();
-        q_phase ^= 1;
-        mbar_arrive_expect_tx(q_full, L::Q_BYTES);
-        const CUtensorMap* tq = it.q_gathered ? &tmQg : &tmQo;
+  if (warp < NWARP_CTRL) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(CTRL_REGS));
+    if (warp == 0) {
+      // ======================= scheduler + Q loader =======================
+      if (elect_one()) {
+        uint32_t q_phase = 0;
+        for (int i = 0;; ++i) {
+          const int slot = i % SCHED_RING;
+          mbar_wait(sched_empty + slot, ((i / SCHED_RING) & 1) ^ 1);
+          int idx = (i == 0) ? (int)blockIdx.x : (int)gridDim.x + (int)atomicAdd(P.sched, 1u);
+          if (idx >= n_items) idx = -1;
+          sched_ring[slot] = idx;
+          mbar_arrive(sched_full + slot);
+          if (idx < 0) break;
+          const ItemView it = load_item(P, idx);
+          if (it.n_tiles <= 0) continue;
+          if (P.dbg) P.dbg[idx * 8 + 0] = gtimer();
+          mbar_wait(q_empty, q_phase ^ 1);
+          q_phase ^= 1;
+          mbar_arrive_expect_tx(q_full, (it.has_b ? 2 : 1) * L::Q_BYTES);
+          const CUtensorMap* tq = it.q_gathered ? &tmQg : &tmQo;
+          for (int hf = 0; hf < (it.has_b ? 2 : 1); ++hf) {
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_2d(smem + L::OFF_Q + c * (BLK * 128), tq, q_full, c * 64, it.q_row0);
-      }
-    }
-  } else if (warp == 2 || warp == 3) {
-    // ======================= K loader (warp 2) / V loader (warp 3) =======================
-    const bool is_k = (warp == 2);
-    if (elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
-      const int NS = is_k ? KST : VST;
-      uint64_t* full = is_k ? k_full : v_full;
-      uint64_t* empty = is_k ? k_empty : v_empty;
-      for (int i = 0;; ++i) {
-        const int idx = fetch(i);
-        mbar_arrive(sched_empty + i % SCHED_RING);
-        if (idx < 0) break;
-        const ItemView it = load_item(P, idx);
-        if (it.n_tiles <= 0) continue;
-        SegIter si;
-        si.init(P, it);
-        for (int t = 0; t < it.n_tiles; ++t) {
-          const TileInfo e = si.next(P, it);
-          mbar_wait(empty + stage, phase ^ 1);
-          uint32_t bytes = L::KV_BYTES;
-          const bool cp_pos = is_k && (e.pred || P.fingerprint) && e.space;
-          const bool cp_rank = is_k && e.pred && e.space && e.rmode;
-          if (cp_pos) bytes += BLK * 4;
-          if (cp_rank) bytes += BLK * 4;
-          mbar_arrive_expect_tx(full + stage, bytes);
-          const CUtensorMap* tm = is_k ? (e.space ? &tmKg : &tmKo) : (e.space ? &tmVg : &tmVo);
-          uint8_t* dst = smem + (is_k ? L::OFF_K : L::OFF_V) + stage * L::KV_BYTES;
-#pragma unroll
-          for (int c = 0; c < D / 64; ++c) tma_load_2d(dst + c * (BLK * 128), tm, full + stage, c * 64, e.krow);
-          if (cp_pos) bulk_load(kpos_s + stage * BLK, P.kg_pos + e.krow, BLK * 4, full + stage);
-          if (cp_rank) bulk_load(krank_s + stage * BLK, P.kg_rank + e.krow, BLK * 4, full + stage);
-          if (++stage == NS) {
-            stage = 0;
-            phase ^= 1;
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_2d(smem + L::OFF_Q + hf * L::Q_BYTES + c * (BLK * 128), tq, q_full, c * 64,
+                          it.q_row0 + hf * BLK);
           }
         }
       }
-    }
-  } else if (warp == 1) {
-    // ======================= MMA issuer (one thread) =======================
-    if (elect_one()) {
-      constexpr uint32_t IDESC_S = idesc_bf16(128, 128, 0);
-      constexpr uint32_t IDESC_O = idesc_bf16(128, D, 1);
-      const uint32_t q_base = smem_u32(smem + L::OFF_Q);
-      const uint32_t k_base = smem_u32(smem + L::OFF_K);
-      const uint32_t v_base = smem_u32(smem + L::OFF_V);
-      int ks = 0, vs = 0, sb = 0;
-      uint32_t k_phase = 0, v_phase = 0, q_phase = 0, o_phase = 0;
-      uint32_t p_phase[2] = {0, 0};
-      for (int i = 0;; ++i) {
-        const int idx = fetch(i);
-        mbar_arrive(sched_empty + i % SCHED_RING);
-        if (idx < 0) break;
-        const ItemView it = load_item(P, idx);
-        if (it.n_tiles <= 0) continue;
-        mbar_wait(q_full, q_phase);
-        if (P.dbg) P.dbg[idx * 8 + 2] = gtimer();
-        q_phase ^= 1;
-        tc_fence_after();
-        int sb_prev = 0;
-        for (int t = 0; t <= it.n_tiles; ++t) {
-          const int sb_cur = sb;
-          if (t < it.n_tiles) {
-            // S[sb] = Q K_t^T.  The buffer's previous P (tile t-2) was consumed by a P V issued
-            // before this MMA; tcgen05.mma executes in issue order.
-            mbar_wait(k_full + ks, k_phase);
-            tc_fence_after();
+    } else if (warp == 2 || warp == 3) {
+      // ======================= K loader (warp 2) / V loader (warp 3) =======================
+      const bool is_k = (warp == 2);
+      if (elect_one()) {
+        int stage = 0;
+        uint32_t phase = 0;
+        const int NS = is_k ? KST : VST;
+        uint64_t* full = is_k ? k_full : v_full;
+        uint64_t* empty = is_k ? k_empty : v_empty;
+        for (int i = 0;; ++i) {
+          const int idx = fetch(i);
+          mbar_arrive(sched_empty + i % SCHED_RING);
+          if (idx < 0) break;
+          const ItemView it = load_item(P, idx);
+          if (it.n_tiles <= 0) continue;
+          SegIter si;
+          si.init(P, it);
+          for (int t = 0; t < it.n_tiles; ++t) {
+            const TileInfo e = si.next(P, it);
+            mbar_wait(empty + stage, phase ^ 1);
+            uint32_t bytes = L::KV_BYTES;
+            const bool cp_pos = is_k && (e.pred || P.fingerprint) && e.space;
+            const bool cp_rank = is_k && e.pred && e.space && e.rmode;
+            if (cp_pos) bytes += BLK * 4;
+            if (cp_rank) bytes += BLK * 4;
+            mbar_arrive_expect_tx(full + stage, bytes);
+            const CUtensorMap* tm = is_k ? (e.space ? &tmKg : &tmKo) : (e.space ? &tmVg : &tmVo);
+            uint8_t* dst = smem + (is_k ? L::OFF_K : L::OFF_V) + stage * L::KV_BYTES;
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c) tma_load_2d(dst + c * (BLK * 128), tm, full + stage, c * 64, e.krow);
+            if (cp_pos) bulk_load(kpos_s + stage * BLK, P.kg_pos + e.krow, BLK * 4, full + stage);
+            if (cp_rank) bulk_load(krank_s + stage * BLK, P.kg_rank + e.krow, BLK * 4, full + stage);
+            if (++stage == NS) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    } else {
+      // ======================= MMA issuer (one thread) =======================
+      if (elect_one()) {
+        constexpr uint32_t IDESC_S = idesc_bf16(128, 128, 0);
+        constexpr uint32_t IDESC_O = idesc_bf16(128, D, 1);
+        const uint32_t q_base = smem_u32(smem + L::OFF_Q);
+        const uint32_t k_base = smem_u32(smem + L::OFF_K);
+        const uint32_t v_base = smem_u32(smem + L::OFF_V);
+        int ks = 0, vs = 0;
+        uint32_t k_phase = 0, v_phase = 0, q_phase = 0;
+        uint32_t p_phase[2] = {0, 0}, o_phase[2] = {0, 0};
+        for (int i = 0;; ++i) {
+          const int idx = fetch(i);
+          mbar_arrive(sched_empty + i % SCHED_RING);
+          if (idx < 0) break;
+          const ItemView it = load_item(P, idx);
+          const int n = it.n_tiles;
+          if (n <= 0) continue;
+          const int nh = it.has_b ? 2 : 1;
+          mbar_wait(q_full, q_phase);
+          q_phase ^= 1;
+          tc_fence_after();
+          // S_h(t) = Q_h K_t^T into the half's S buffer (its previous P was consumed by
+          // a P V issued earlier; tcgen05.mma executes in issue order)
+          auto issue_s = [&](int hf, int t) {
 #pragma unroll
             for (int k = 0; k < D / 16; ++k) {
               const uint32_t off = (k / 4) * (BLK * 128) + (k % 4) * 32;
-              const uint64_t ad = smem_desc(q_base + off, 16, 1024, 2);
+              const uint64_t ad = smem_desc(q_base + hf * L::Q_BYTES + off, 16, 1024, 2);
               const uint64_t bd = smem_desc(k_base + ks * L::KV_BYTES + off, 16, 1024, 2);
-              umma_ss(tS[sb], ad, bd, IDESC_S, k > 0 ? 1u : 0u);
+              umma_ss(tmem + 128 * hf, ad, bd, IDESC_S, k > 0 ? 1u : 0u);
             }
-            umma_commit(s_full + sb);
-            umma_commit(k_empty + ks);
-            if (t == it.n_tiles - 1) umma_commit(q_empty);
-            sb ^= 1;
-            if (++ks == KST) {
-              ks = 0;
-              k_phase ^= 1;
+            umma_commit(s_full + hf);
+            if (hf == nh - 1) {
+              umma_commit(k_empty + ks);  // K(t) consumed by every half
+              if (t == n - 1) umma_commit(q_empty);
             }
-          }
-          if (t >= 1) {
-            // O += P_{t-1} V_{t-1}, P read from TMEM (aliasing S buffer sb_prev)
-            mbar_wait(p_full + sb_prev, p_phase[sb_prev]);
-            p_phase[sb_prev] ^= 1;
-            if (t == 1) mbar_wait(o_empty, o_phase ^ 1);  // previous item's epilogue has read O
-            mbar_wait(v_full + vs, v_phase);
+          };
+          // O_h += P_h(t) V_t, P read from TMEM (A operand)
+          auto issue_pv = [&](int hf, int t) {
+            mbar_wait(p_full + hf, p_phase[hf]);
+            p_phase[hf] ^= 1;
+            if (t == 0) mbar_wait(o_empty + hf, o_phase[hf] ^ 1);  // previous item's epilogue read O_h
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < BLK / 16; ++k) {
               const uint64_t bd = smem_desc(v_base + vs * L::KV_BYTES + k * 2048, BLK * 128, 1024, 2);
-              umma_ts(tO, tS[sb_prev] + k * 8, bd, IDESC_O, (t > 1 || k > 0) ? 1u : 0u);
+              umma_ts(tmem + 256 + 128 * hf, tmem + 128 * hf + k * 8, bd, IDESC_O, (t > 0 || k > 0) ? 1u : 0u);
+            }
+            if (t == n - 1) {
+              umma_commit(o_full + hf);
+              o_phase[hf] ^= 1;
+            }
+          };
+          // prologue: S of tile 0 for every half
+          mbar_wait(k_full + ks, k_phase);
+          tc_fence_after();
+          for (int hf = 0; hf < nh; ++hf) issue_s(hf, 0);
+          if (++ks == KST) {
+            ks = 0;
+            k_phase ^= 1;
+          }
+          for (int t = 0; t < n; ++t) {
+            mbar_wait(v_full + vs, v_phase);
+            const bool more = (t + 1 < n);
+            // half A: P V(t), then S(t+1) while half B's softmax still runs
+            issue_pv(0, t);
+            if (more) {
+              mbar_wait(k_full + ks, k_phase);
+              tc_fence_after();
+              issue_s(0, t + 1);
+            }
+            if (nh == 2) {
+              issue_pv(1, t);
+              if (more) issue_s(1, t + 1);
             }
             umma_commit(v_empty + vs);
-            umma_commit(pv_done);
-            if (t == it.n_tiles) umma_commit(o_full);
             if (++vs == VST) {
               vs = 0;
               v_phase ^= 1;
             }
+            if (more && ++ks == KST) {
+              ks = 0;
+              k_phase ^= 1;
+            }
           }
-          sb_prev = sb_cur;
         }
-        o_phase ^= 1;
       }
     }
-  } else if (warp >= 4) {
-    // ======================= softmax / correction / epilogue =======================
-    const int row = threadIdx.x - 128;                 // TMEM lane == query row
-    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SOFT_REGS));
+    // ======================= softmax / correction / epilogue (one warpgroup per half) =======================
+    const int hf = (warp - NWARP_CTRL) / 4;          // half of the item this warpgroup owns
+    const int row = (threadIdx.x - 32 * NWARP_CTRL) % 128;  // TMEM lane == row of the half
+    const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
+    const uint32_t tS = tmem + 128 * hf + lane_off;
+    const uint32_t tO = tmem + 256 + 128 * hf + lane_off;
     int stage = 0;  // K ring stage (key coordinates)
-    uint32_t kv_phase = 0, o_phase = 0;
-    uint32_t s_phase[2] = {0, 0};
-    int sbuf = 0;
-    long long pv_count = 0;  // P V MMAs issued so far by this CTA (phase index of pv_done)
+    uint32_t kv_phase = 0, s_phase = 0, o_phase = 0;
     const int G = P.H / P.Hkv;
     for (int i = 0;; ++i) {
       const int idx = fetch(i);
@@ -414,14 +448,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (idx < 0) break;
       const ItemView it = load_item(P, idx);
       if (it.n_tiles <= 0) continue;  // empty slot: nothing to compute or write
-      if (P.dbg && row == 0) P.dbg[idx * 8 + 3] = gtimer();
+      if (hf == 1 && !it.has_b) {
+        // absent half: only release the key-coordinate stages
+        for (int t = 0; t < it.n_tiles; ++t) {
+          mbar_wait(k_full + stage, kv_phase);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(k_empty + stage);
+          if (++stage == KST) {
+            stage = 0;
+            kv_phase ^= 1;
+          }
+        }
+        continue;
+      }
+      if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 3] = gtimer();
       // row identity
+      const int qrow = it.q_row0 + hf * BLK + row;
       int xpos, xrank;
       if (it.q_gathered) {
-        xpos = P.qg_pos[it.q_row0 + row];
-        xrank = P.qg_rank[it.q_row0 + row];
+        xpos = P.qg_pos[qrow];
+        xrank = P.qg_rank[qrow];
       } else {
-        xpos = it.q_row0 - it.head * P.S + row;
+        xpos = qrow - it.head * P.S;
         xrank = (xpos < P.S && P.rank) ? P.rank[xpos] : xpos;
       }
       bool valid = xpos >= 0 && xpos < P.S;
@@ -439,15 +487,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int t = 0; t < it.n_tiles; ++t) {
         const TileInfo e = si.next(P, it);
         const uint32_t space = e.space, pred = e.pred, role = e.role, rmode = e.rmode, inst = e.inst;
-        mbar_wait(s_full + sbuf, s_phase[sbuf]);
-        if (P.dbg && row == 0 && t == 0) P.dbg[idx * 8 + 7] = gtimer();
-        s_phase[sbuf] ^= 1;
+        mbar_wait(s_full + hf, s_phase);
+        s_phase ^= 1;
         tc_fence_after();
         float s[BLK];
 #pragma unroll
         for (int c = 0; c < BLK / 32; ++c) {
           uint32_t r[32];
-          tmem_ld32(tS[sbuf] + lane_off + c * 32, r);
+          tmem_ld32(tS + c * 32, r);
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(r[j]);  // raw scores
@@ -507,7 +554,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
             if (P.fingerprint) {
-#pragma unroll 1
+#pragma unroll
               for (int w = 0; w < 4; ++w) {
                 uint32_t bitsw = mw[w];
                 while (bitsw) {
@@ -554,40 +601,35 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           pk[c / 2] = pack_bf16(p0, p1);
         }
         l_sum = l_sum * alpha + ls;
-        // O correction: only when the running max moved; needs the previous P V complete
+        // O correction only when the running max moved; O_h is quiescent: P V_h(t-1) was
+        // issued before S_h(t), which has completed.
         if (t > 0 && __any_sync(0xffffffffu, rescale)) {
-          mbar_wait(pv_done, (uint32_t)((pv_count + t - 1) & 1));
-          tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t r[32];
-            tmem_ld32(tO + lane_off + c * 32, r);
+            tmem_ld32(tO + c * 32, r);
             tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
-            tmem_st32(tO + lane_off + c * 32, r);
+            tmem_st32(tO + c * 32, r);
           }
         }
-        // P (bf16 pairs) -> TMEM columns [0, 64) of this S buffer: the A operand of P V
-        tmem_st32(tS[sbuf] + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-        tmem_st32(tS[sbuf] + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        // P (bf16 pairs) -> TMEM columns [0, 64) of this half's S buffer
+        tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(p_full + sbuf);
-        sbuf ^= 1;
+        mbar_arrive(p_full + hf);
       }
-      pv_count += it.n_tiles;
       // ---- epilogue ----
-      if (P.dbg && row == 0) P.dbg[idx * 8 + 4] = gtimer();
-      mbar_wait(o_full, o_phase);
+      mbar_wait(o_full + hf, o_phase);
       o_phase ^= 1;
       tc_fence_after();
-      if (P.dbg && row == 0) P.dbg[idx * 8 + 5] = gtimer();
       const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
       const float lse_v = l_sum > 0.f ? (m_used + __log2f(l_sum)) * 0.6931471805599453f : -INFINITY;
       if (P.fingerprint) {
         tc_fence_before();
-        mbar_arrive(o_empty);
+        mbar_arrive(o_empty + hf);
         if (write) {
           long long* f = reinterpret_cast<long long*>(P.fp_out) + 3ll * ((long long)it.head * P.S + xpos);
           atomicAdd(reinterpret_cast<unsigned long long*>(f + 0), (unsigned long long)fp_cnt);
@@ -601,11 +643,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
-          tmem_ld32(tO + lane_off + c * 32, r);
+          tmem_ld32(tO + c * 32, r);
           tmem_wait_ld();
           if (c == D / 32 - 1) {
             tc_fence_before();
-            mbar_arrive(o_empty);  // O fully in registers: the next item's first P V may start
+            mbar_arrive(o_empty + hf);  // O in registers: the next item's first P V may start
           }
           if (write) {
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
@@ -622,15 +664,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         if (write && P.lse) P.lse[(size_t)it.head * P.S + xpos] = lse_v;
       } else {
-        float* prow = P.part_o + (size_t)(it.out_row0 + row) * D;
+        float* prow = P.part_o + (size_t)(it.out_row0 + hf * BLK + row) * D;
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
-          tmem_ld32(tO + lane_off + c * 32, r);
+          tmem_ld32(tO + c * 32, r);
           tmem_wait_ld();
           if (c == D / 32 - 1) {
             tc_fence_before();
-            mbar_arrive(o_empty);
+            mbar_arrive(o_empty + hf);
           }
           float4* dst = reinterpret_cast<float4*>(prow + c * 32);
 #pragma unroll
@@ -638,9 +680,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             dst[j] = make_float4(__uint_as_float(r[4 * j]) * inv_l, __uint_as_float(r[4 * j + 1]) * inv_l,
                                  __uint_as_float(r[4 * j + 2]) * inv_l, __uint_as_float(r[4 * j + 3]) * inv_l);
         }
-        P.part_lse[it.out_row0 + row] = valid ? lse_v : -INFINITY;
+        P.part_lse[it.out_row0 + hf * BLK + row] = valid ? lse_v : -INFINITY;
       }
-      if (P.dbg && row == 0) P.dbg[idx * 8 + 6] = gtimer();
+      if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 6] = gtimer();
     }
   }
   tc_fence_before();
@@ -706,7 +748,7 @@ cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hi
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int grid = g_num_sms;
-  if (n_items_hint > 0 && n_items_hint < grid) grid = n_items_hint;
+  if (n_items_hint > 0 && (n_items_hint + 1) / 2 < grid) grid = (n_items_hint + 1) / 2;
   if (grid <= 0) return cudaSuccess;
   AttnParams Pl = P;
   if (!Pl.sched) {

@@ -487,31 +487,47 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
   W.inst_base = I.h * MAX_INST;
   W.skip_s = W.skip_p = W.skip_rank = 0;
   W.row_mod = -1;
-  W.pad[0] = W.pad[1] = W.pad[2] = 0;
+  W.has_b = 0;
+  W.pad[0] = W.pad[1] = 0;
   RowsInfo R;
   if (ps.pass == PASS_MAIN) {
     int grp;
+    int row_in_view;  // first row of block A in the MAIN view (partial-buffer row)
     if (hd.qmod_view < 0) {
-      const int p0 = b * BLK;
+      const int p0 = 2 * b * BLK;
       if (p0 >= C.S) return;
       R.xp_lo = p0;
-      R.xp_hi = min(C.S, p0 + BLK) - 1;
+      R.xp_hi = min(C.S, p0 + 2 * BLK) - 1;
       R.xr_lo = R.xr_hi = 0;
       W.q_row0 = I.h * C.S + p0;
+      W.has_b = (p0 + BLK < C.S) ? 1 : 0;
+      row_in_view = p0;
       grp = 0;
     } else {
-      const int i0 = b * BLK;
-      if (i0 >= C.info[MI_PADOFF + MAX_MOD]) return;
+      // pair b inside modality group m (blocks of a group never pair across groups)
+      int k = b, a = -1, kk = 0, nblk = 0;
+      for (int m = 0; m < MAX_MOD; ++m) {
+        nblk = (C.info[MI_CNT + m] + BLK - 1) / BLK;
+        const int pairs = (nblk + 1) / 2;
+        if (k < pairs) {
+          a = m;
+          kk = k;
+          break;
+        }
+        k -= pairs;
+      }
+      if (a < 0) return;
+      const int i0 = C.info[MI_PADOFF + a] + 2 * kk * BLK;
+      const int ilast = min(i0 + 2 * BLK - 1, C.info[MI_PADOFF + a] + C.info[MI_CNT + a] - 1);
       const int p0 = C.modpos[i0];
-      if (p0 < 0) return;
-      const int a = C.labels[p0];
-      const int ilast = min(i0 + BLK - 1, C.info[MI_PADOFF + a] + C.info[MI_CNT + a] - 1);
       R.xp_lo = p0;
       R.xp_hi = C.modpos[ilast];
       R.xr_lo = C.rank[p0];
       R.xr_hi = C.rank[R.xp_hi];
       W.q_row0 = C.views[hd.qmod_view].row_off + i0;
       W.q_gathered = 1;
+      W.has_b = (2 * kk + 1 < nblk) ? 1 : 0;
+      row_in_view = i0;
       grp = a;
     }
     // skip rows owned by the HROW pass; partial output when the group has a slash pass
@@ -528,7 +544,7 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
     }
     if (hd.sl_inst[grp] >= 0) {
       W.out_mode = OUT_PARTIAL;
-      W.out_row0 = hd.part_rows0 + b * BLK;
+      W.out_row0 = hd.part_rows0 + row_in_view;
     }
     W.pad[0] = R.xp_lo;
     for (int ii = 0; ii < hd.n_inst; ++ii) {
@@ -542,26 +558,40 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
     const GridRes g = C.gridres[x.grid_id];
     const int n = x.rank ? C.info[MI_CNT + x.qa] : C.S;
     const int* P_a = x.rank ? C.perm + C.info[MI_OFF + x.qa] : nullptr;
-    int r, t0;
+    int r, t0, nr;
     if (ps.pass == PASS_HROW) {
       r = g.p;
-      t0 = b * BLK;
+      nr = r < n ? (n - r + g.s - 1) / g.s : 0;
+      t0 = 2 * b * BLK;
       const DView qv = C.views[x.v_cls_q];
       W.q_row0 = qv.row_off + t0;
     } else {
+      // pair b inside residue class r: classes r < rem hold q+1 keys, the others q
       ClassGeo cg;
       cg.init(n, g.s);
-      if (!cg.locate(b * BLK, r, t0)) return;
-      if (b * BLK >= cg.total()) return;
+      const int pa = ((cg.q + 1 + BLK - 1) / BLK + 1) / 2, pb = ((cg.q + BLK - 1) / BLK + 1) / 2;
+      int kk;
+      if (b < cg.rem * pa) {
+        r = b / pa;
+        kk = b % pa;
+      } else {
+        if (pb == 0) return;
+        r = cg.rem + (b - cg.rem * pa) / pb;
+        kk = (b - cg.rem * pa) % pb;
+        if (r >= g.s) return;
+      }
       if (r == g.p && (x.flags & (GF_H | GF_V))) return;  // class p owned by H / V passes (C9)
+      nr = cg.nr(r);
+      t0 = 2 * kk * BLK;
+      const int res_row = cg.classoff(r) + t0;
       const DView qv = C.views[x.v_res_q];
-      W.q_row0 = qv.row_off + b * BLK;
+      W.q_row0 = qv.row_off + res_row;
       W.out_mode = OUT_PARTIAL;
-      W.out_row0 = x.pad[0] + b * BLK;
+      W.out_row0 = x.pad[0] + res_row;
     }
-    const int nr = r < n ? (n - r + g.s - 1) / g.s : 0;
     if (t0 >= nr) return;
-    const int tl = min(t0 + BLK - 1, nr - 1);
+    W.has_b = (t0 + BLK < nr) ? 1 : 0;
+    const int tl = min(t0 + 2 * BLK - 1, nr - 1);
     const int c_lo = r + g.s * t0, c_hi = r + g.s * tl;
     W.q_gathered = 1;
     W.row_mod = ps.qa;

@@ -52,7 +52,8 @@ struct WorkItem {
   int32_t skip_p;     //     (hline rows owned by the HROW pass, reading C9)
   int32_t skip_rank;  //     coord system of the skip test
   int32_t row_mod;    // >=0: only rows of this modality are valid (Q-boundary class views)
-  int32_t pad[3];
+  int32_t has_b;      // 1: the item also covers the next 128-row block (rows q_row0 + 128 ...)
+  int32_t pad[2];
 };
 
 struct AttnParams {

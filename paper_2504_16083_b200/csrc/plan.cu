@@ -226,7 +226,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
       case MMI_PAT_FULL: return 1;
       case MMI_PAT_ASHAPE: return 2;
       case MMI_PAT_GRID: return 3;
-      case MMI_PAT_VSLASH: return 1 + std::min<int64_t>((int64_t)x.n_s + 1, nbk_max / 2 + 2);
+      case MMI_PAT_VSLASH: return 1 + std::min<int64_t>(2 * (int64_t)x.n_s + 2, nbk_max / 2 + 2);
       default: return 0;
     }
   };
@@ -242,7 +242,8 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
     mp.pass = PASS_MAIN;
     mp.inst = -1;
     mp.qa = -1;
-    mp.n_slots = modq ? (int)(mod_cap / BLK) : P.nb;
+    // work items are pairs of 128-row blocks of one group (modality / residue class)
+    mp.n_slots = modq ? (int)((mod_cap / BLK + 1) / 2 + M) : (P.nb + 1) / 2;
     mp.slot_base = slot;
     slot += mp.n_slots;
     P.passes.push_back(mp);
@@ -272,7 +273,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
         p2.pass = PASS_HROW;
         p2.inst = i;
         p2.qa = (hd.boundary == MMI_BND_Q) ? x.qa : -1;
-        p2.n_slots = P.views[x.v_cls_q].cap / BLK;
+        p2.n_slots = (P.views[x.v_cls_q].cap / BLK + 1) / 2 + 1;
         p2.slot_base = slot;
         slot += p2.n_slots;
         P.passes.push_back(p2);
@@ -285,7 +286,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
         p3.pass = PASS_SLASH;
         p3.inst = i;
         p3.qa = (hd.boundary == MMI_BND_Q) ? x.qa : -1;
-        p3.n_slots = P.views[x.v_res_q].cap / BLK;
+        p3.n_slots = (P.views[x.v_res_q].cap / BLK + 1) / 2 + x.smax + 1;
         p3.slot_base = slot;
         slot += p3.n_slots;
         P.passes.push_back(p3);

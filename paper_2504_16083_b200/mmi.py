@@ -16,7 +16,7 @@ import torch
 from synth.config import HeadConfig, Pattern, Problem, MAX_MOD
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmmi.so")
+LIB_PATH = os.environ.get("MMI_LIB") or os.path.join(_HERE, "libmmi.so")  # MMI_LIB: an alternative in-tree build
 
 MMI_OK = 0
 STATUS = {0: "MMI_OK", 1: "MMI_E_INVALID", 2: "MMI_E_SHAPE", 3: "MMI_E_CONFIG", 4: "MMI_E_UNSUPPORTED",
