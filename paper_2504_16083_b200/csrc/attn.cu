@@ -33,26 +33,51 @@
 namespace mmi {
 
 constexpr float RESCALE_THRESH = 8.0f;  // lazy rescale: P <= 2^8 (log2 domain)
+// column pairs (bit i of each group of 8 pairs) whose exp2 runs as a polynomial on the FMA pipe
+// instead of MUFU.EX2: MUFU is 4 lanes/clk per SM sub-partition, so 128 exp2 per row and tile
+// would otherwise take longer than the other half's two MMAs they must hide behind
+#ifndef MMI_EMU_MASK
+#define MMI_EMU_MASK 0x11u
+#endif
+constexpr uint32_t EMU_MASK = MMI_EMU_MASK;
 
 // Work items cover two 128-row query blocks (halves A and B); each half has its
-// own softmax warpgroup, TMEM S/P buffer (128 columns) and O accumulator (128
-// columns): 512 columns total.  K/V tiles are shared by both halves.
+// own softmax warpgroup, TMEM S/P buffer (128 columns = two 64-key sub-tile
+// slots) and O accumulator (128 columns): 512 columns total.  K/V tiles are
+// shared by both halves.
 template <int D>
 struct Cfg {
   static constexpr int KST = (D == 128) ? 2 : 3;  // K ring stages
   static constexpr int VST = (D == 128) ? 2 : 3;  // V ring stages
 };
 constexpr int SCHED_RING = 4;
-constexpr int NWARP_CTRL = 4;                     // scheduler+Q, MMA, K loader, V loader
-constexpr int NTHREADS = 32 * (NWARP_CTRL + 8);  // + two softmax warpgroups
-constexpr int LAUNCH_REGS = 168;                  // ptxas allocation at __launch_bounds__(384, 1)
+constexpr int NWARP_CTRL = 4;                      // scheduler+Q, MMA, K loader, V loader
+constexpr int NWARP_SOFT = 8;                      // 2 softmax warpgroups: one per query half
+constexpr int NTHREADS = 32 * (NWARP_CTRL + NWARP_SOFT);
+constexpr int LAUNCH_REGS = 168;                   // ptxas allocation at __launch_bounds__(384, 1)
 #ifndef MMI_CTRL_REGS
-#define MMI_CTRL_REGS 56
-#define MMI_SOFT_REGS 224
+#define MMI_CTRL_REGS 96
+#define MMI_SOFT_REGS 200
 #endif
-constexpr int CTRL_REGS = MMI_CTRL_REGS;                    // setmaxnreg budgets: .inc only draws on what .dec released
-constexpr int SOFT_REGS = MMI_SOFT_REGS;                    // inside the CTA's launch allocation (384*168), else it blocks forever
-static_assert(128 * CTRL_REGS + 256 * SOFT_REGS <= NTHREADS * LAUNCH_REGS, "setmaxnreg budget exceeds launch allocation");
+constexpr int CTRL_REGS = MMI_CTRL_REGS;  // setmaxnreg budgets: .inc only draws on what .dec released
+constexpr int SOFT_REGS = MMI_SOFT_REGS;  // inside the CTA's launch allocation, else it blocks forever
+static_assert(32 * NWARP_CTRL * CTRL_REGS + 32 * NWARP_SOFT * SOFT_REGS <= NTHREADS * LAUNCH_REGS,
+              "setmaxnreg budget exceeds launch allocation");
+constexpr int NKP = 4;  // key-coordinate ring (positions / ranks of gathered key tiles that need them)
+
+// MMI_PROF builds (scratch/variants.sh only) accumulate per-phase SM clocks into g_prof
+#ifdef MMI_PROF
+__device__ unsigned long long g_prof[32];
+#define PROF_DECL(n) long long prof_##n = 0
+#define PROF_T() clock64()
+#define PROF_ADD(n, t0) prof_##n += clock64() - (t0)
+#define PROF_FLUSH(i, n) atomicAdd(&g_prof[i], (unsigned long long)prof_##n)
+#else
+#define PROF_DECL(n)
+#define PROF_T() 0ll
+#define PROF_ADD(n, t0)
+#define PROF_FLUSH(i, n)
+#endif
 
 template <int D>
 struct Smem {
@@ -63,12 +88,12 @@ struct Smem {
   static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
   static constexpr int OFF_KPOS = OFF_V + VST * KV_BYTES;
-  static constexpr int OFF_KRANK = OFF_KPOS + KST * BLK * 4;
-  static constexpr int OFF_SCHED = OFF_KRANK + KST * BLK * 4;
+  static constexpr int OFF_KRANK = OFF_KPOS + NKP * BLK * 4;
+  static constexpr int OFF_SCHED = OFF_KRANK + NKP * BLK * 4;
   static constexpr int OFF_BAR = OFF_SCHED + 64;
-  // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2] p_full[2] o_full[2] o_empty[2]
-  // sched_full[R] sched_empty[R]
-  static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 8 + 2 * SCHED_RING;
+  // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2][2] p_full[2][2] o_full[2]
+  // o_empty[2] pv_done[2] sched_full[R] sched_empty[R] kp_full[NKP] kp_empty[NKP]
+  static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 14 + 2 * SCHED_RING + 2 * NKP;
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
   static constexpr int TOTAL = OFF_TMEM + 16;
   static constexpr int ALLOC = TOTAL + 1024;  // alignment slack
@@ -215,12 +240,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* k_empty = k_full + KST;
   uint64_t* v_full = k_empty + KST;
   uint64_t* v_empty = v_full + VST;
-  uint64_t* s_full = v_empty + VST;  // [2] per half: S written by the MMA
-  uint64_t* p_full = s_full + 2;     // [2] per half: P (bf16, aliasing S in TMEM) written by the softmax
-  uint64_t* o_full = p_full + 2;     // [2] per half
-  uint64_t* o_empty = o_full + 2;    // [2] per half
-  uint64_t* sched_full = o_empty + 2;
+  uint64_t* s_full = v_empty + VST;  // [half][slot]: S of a 64-key sub-tile written by the MMA
+  uint64_t* p_full = s_full + 4;     // [half][slot]: P (bf16, aliasing S in TMEM) written by the softmax
+  uint64_t* o_full = p_full + 4;     // [half]
+  uint64_t* o_empty = o_full + 2;    // [half]
+  uint64_t* pv_done = o_empty + 2;   // [half]: one commit per P V
+  uint64_t* sched_full = pv_done + 2;
   uint64_t* sched_empty = sched_full + SCHED_RING;
+  uint64_t* kp_full = sched_empty + SCHED_RING;
+  uint64_t* kp_empty = kp_full + NKP;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
   int32_t* kpos_s = reinterpret_cast<int32_t*>(smem + L::OFF_KPOS);
   int32_t* krank_s = reinterpret_cast<int32_t*>(smem + L::OFF_KRANK);
@@ -234,21 +262,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_init(q_empty, 1);
     for (int i = 0; i < KST; ++i) {
       mbar_init(k_full + i, 1);
-      mbar_init(k_empty + i, 1 + 8);  // last S-MMA commit + one arrival per softmax warp (key coords consumed)
+      mbar_init(k_empty + i, 1);  // last S-MMA commit
     }
     for (int i = 0; i < VST; ++i) {
       mbar_init(v_full + i, 1);
       mbar_init(v_empty + i, 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 128);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(o_full + i, 1);
       mbar_init(o_empty + i, 128);
+      mbar_init(pv_done + i, 1);
     }
     for (int i = 0; i < SCHED_RING; ++i) {
       mbar_init(sched_full + i, 1);
-      mbar_init(sched_empty + i, 3 + 8);  // K loader, V loader, MMA, 8 softmax warps
+      mbar_init(sched_empty + i, 3 + NWARP_SOFT);  // K loader, V loader, MMA, softmax warps
+    }
+    for (int i = 0; i < NKP; ++i) {
+      mbar_init(kp_full + i, 1);
+      mbar_init(kp_empty + i, NWARP_SOFT);  // one arrival per softmax warp
     }
     fence_barrier_init();
   }
@@ -306,8 +341,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // ======================= K loader (warp 2) / V loader (warp 3) =======================
       const bool is_k = (warp == 2);
       if (elect_one()) {
-        int stage = 0;
-        uint32_t phase = 0;
+        int stage = 0, kps = 0;
+        uint32_t phase = 0, kp_phase = 0;
         const int NS = is_k ? KST : VST;
         uint64_t* full = is_k ? k_full : v_full;
         uint64_t* empty = is_k ? k_empty : v_empty;
@@ -322,18 +357,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int t = 0; t < it.n_tiles; ++t) {
             const TileInfo e = si.next(P, it);
             mbar_wait(empty + stage, phase ^ 1);
-            uint32_t bytes = L::KV_BYTES;
-            const bool cp_pos = is_k && (e.pred || P.fingerprint) && e.space;
-            const bool cp_rank = is_k && e.pred && e.space && e.rmode;
-            if (cp_pos) bytes += BLK * 4;
-            if (cp_rank) bytes += BLK * 4;
-            mbar_arrive_expect_tx(full + stage, bytes);
+            mbar_arrive_expect_tx(full + stage, L::KV_BYTES);
             const CUtensorMap* tm = is_k ? (e.space ? &tmKg : &tmKo) : (e.space ? &tmVg : &tmVo);
             uint8_t* dst = smem + (is_k ? L::OFF_K : L::OFF_V) + stage * L::KV_BYTES;
 #pragma unroll
             for (int c = 0; c < D / 64; ++c) tma_load_2d(dst + c * (BLK * 128), tm, full + stage, c * 64, e.krow);
-            if (cp_pos) bulk_load(kpos_s + stage * BLK, P.kg_pos + e.krow, BLK * 4, full + stage);
-            if (cp_rank) bulk_load(krank_s + stage * BLK, P.kg_rank + e.krow, BLK * 4, full + stage);
+            // key coordinates of gathered tiles the softmax masks or fingerprints (same predicate there)
+            const bool cp_pos = is_k && (e.pred || P.fingerprint) && e.space;
+            if (cp_pos) {
+              const bool cp_rank = e.pred && e.rmode;
+              mbar_wait(kp_empty + kps, kp_phase ^ 1);
+              mbar_arrive_expect_tx(kp_full + kps, (cp_rank ? 2 : 1) * BLK * 4);
+              bulk_load(kpos_s + kps * BLK, P.kg_pos + e.krow, BLK * 4, kp_full + kps);
+              if (cp_rank) bulk_load(krank_s + kps * BLK, P.kg_rank + e.krow, BLK * 4, kp_full + kps);
+              if (++kps == NKP) {
+                kps = 0;
+                kp_phase ^= 1;
+              }
+            }
             if (++stage == NS) {
               stage = 0;
               phase ^= 1;
@@ -343,15 +384,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     } else {
       // ======================= MMA issuer (one thread) =======================
+      // Sub-tile j = 2t + u covers keys [64u, 64u + 64) of key tile t.  S_h(j) goes to slot u
+      // (TMEM columns [64u, 64u + 64) of half h's S buffer) and P_h(j) overwrites its first 32
+      // columns, so S_h(j + 1) (other slot) is issued before P_h(j) V: the softmax of a half
+      // always finds its next scores ready and runs back to back.
       if (elect_one()) {
-        constexpr uint32_t IDESC_S = idesc_bf16(128, 128, 0);
+        constexpr uint32_t IDESC_S = idesc_bf16(128, 64, 0);
         constexpr uint32_t IDESC_O = idesc_bf16(128, D, 1);
         const uint32_t q_base = smem_u32(smem + L::OFF_Q);
         const uint32_t k_base = smem_u32(smem + L::OFF_K);
         const uint32_t v_base = smem_u32(smem + L::OFF_V);
         int ks = 0, vs = 0;
         uint32_t k_phase = 0, v_phase = 0, q_phase = 0;
-        uint32_t p_phase[2] = {0, 0}, o_phase[2] = {0, 0};
+        uint32_t p_phase[4] = {0, 0, 0, 0}, o_phase[2] = {0, 0};
+        PROF_DECL(wp); PROF_DECL(wk); PROF_DECL(wv); PROF_DECL(wq); PROF_DECL(wo); PROF_DECL(tot); PROF_DECL(nt);
+        [[maybe_unused]] const long long prof_start = PROF_T();
         for (int i = 0;; ++i) {
           const int idx = fetch(i);
           mbar_arrive(sched_empty + i % SCHED_RING);
@@ -360,89 +407,122 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int n = it.n_tiles;
           if (n <= 0) continue;
           const int nh = it.has_b ? 2 : 1;
+          const int nsub = 2 * n;
+          long long t0 = PROF_T();
           mbar_wait(q_full, q_phase);
+          PROF_ADD(wq, t0);
           q_phase ^= 1;
           tc_fence_after();
-          // S_h(t) = Q_h K_t^T into the half's S buffer (its previous P was consumed by
-          // a P V issued earlier; tcgen05.mma executes in issue order)
-          auto issue_s = [&](int hf, int t) {
+          // S_h(j) = Q_h K(j)^T, 64 keys, K stage kst
+          auto issue_s = [&](int hf, int j, int kst) {
+            const int u = j & 1;
 #pragma unroll
             for (int k = 0; k < D / 16; ++k) {
               const uint32_t off = (k / 4) * (BLK * 128) + (k % 4) * 32;
               const uint64_t ad = smem_desc(q_base + hf * L::Q_BYTES + off, 16, 1024, 2);
-              const uint64_t bd = smem_desc(k_base + ks * L::KV_BYTES + off, 16, 1024, 2);
-              umma_ss(tmem + 128 * hf, ad, bd, IDESC_S, k > 0 ? 1u : 0u);
+              const uint64_t bd = smem_desc(k_base + kst * L::KV_BYTES + u * 64 * 128 + off, 16, 1024, 2);
+              umma_ss(tmem + 128 * hf + 64 * u, ad, bd, IDESC_S, k > 0 ? 1u : 0u);
             }
-            umma_commit(s_full + hf);
-            if (hf == nh - 1) {
-              umma_commit(k_empty + ks);  // K(t) consumed by every half
-              if (t == n - 1) umma_commit(q_empty);
-            }
+            umma_commit(s_full + 2 * hf + u);
+            if (j == nsub - 1 && hf == nh - 1) umma_commit(q_empty);  // last S of the item
           };
-          // O_h += P_h(t) V_t, P read from TMEM (A operand)
-          auto issue_pv = [&](int hf, int t) {
-            mbar_wait(p_full + hf, p_phase[hf]);
-            p_phase[hf] ^= 1;
-            if (t == 0) mbar_wait(o_empty + hf, o_phase[hf] ^ 1);  // previous item's epilogue read O_h
+          // O_h += P_h(j) V(j), P read from TMEM (A operand), V stage vs
+          auto issue_pv = [&](int hf, int j) {
+            const int u = j & 1;
+            long long t0 = PROF_T();
+            mbar_wait(p_full + 2 * hf + u, p_phase[2 * hf + u]);
+            PROF_ADD(wp, t0);
+            p_phase[2 * hf + u] ^= 1;
+            t0 = PROF_T();
+            if (j == 0) mbar_wait(o_empty + hf, o_phase[hf] ^ 1);  // previous item's epilogue read O_h
+            PROF_ADD(wo, t0);
             tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < BLK / 16; ++k) {
-              const uint64_t bd = smem_desc(v_base + vs * L::KV_BYTES + k * 2048, BLK * 128, 1024, 2);
-              umma_ts(tmem + 256 + 128 * hf, tmem + 128 * hf + k * 8, bd, IDESC_O, (t > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t bd = smem_desc(v_base + vs * L::KV_BYTES + (4 * u + k) * 2048, BLK * 128, 1024, 2);
+              umma_ts(tmem + 256 + 128 * hf, tmem + 128 * hf + 64 * u + k * 8, bd, IDESC_O,
+                      (j > 0 || k > 0) ? 1u : 0u);
             }
-            if (t == n - 1) {
+            umma_commit(pv_done + hf);  // lets the softmax rescale O_h once this P V has landed
+            if (j == nsub - 1) {
               umma_commit(o_full + hf);
               o_phase[hf] ^= 1;
             }
           };
-          // prologue: S of tile 0 for every half
+          // prologue: both sub-tiles of key tile 0 for every half
+          t0 = PROF_T();
           mbar_wait(k_full + ks, k_phase);
+          PROF_ADD(wk, t0);
           tc_fence_after();
-          for (int hf = 0; hf < nh; ++hf) issue_s(hf, 0);
+          for (int j = 0; j < 2; ++j)
+            for (int hf = 0; hf < nh; ++hf) issue_s(hf, j, ks);
+          umma_commit(k_empty + ks);
           if (++ks == KST) {
             ks = 0;
             k_phase ^= 1;
           }
-          for (int t = 0; t < n; ++t) {
-            mbar_wait(v_full + vs, v_phase);
-            const bool more = (t + 1 < n);
-            // half A: P V(t), then S(t+1) while half B's softmax still runs
-            issue_pv(0, t);
-            if (more) {
-              mbar_wait(k_full + ks, k_phase);
-              tc_fence_after();
-              issue_s(0, t + 1);
+          for (int j = 0; j < nsub; ++j) {
+            const int u = j & 1;
+            const bool ahead = (j + 2 < nsub);  // S of sub-tile j + 2 (key tile t + 1, stage ks)
+            if (u == 0) {
+              t0 = PROF_T();
+              mbar_wait(v_full + vs, v_phase);
+              PROF_ADD(wv, t0);
+              if (ahead) {
+                t0 = PROF_T();
+                mbar_wait(k_full + ks, k_phase);
+                PROF_ADD(wk, t0);
+                tc_fence_after();
+              }
             }
-            if (nh == 2) {
-              issue_pv(1, t);
-              if (more) issue_s(1, t + 1);
+#ifdef MMI_PROF
+            prof_nt += nh;
+#endif
+            for (int hf = 0; hf < nh; ++hf) {
+              issue_pv(hf, j);
+              if (ahead) issue_s(hf, j + 2, ks);
             }
-            umma_commit(v_empty + vs);
-            if (++vs == VST) {
-              vs = 0;
-              v_phase ^= 1;
-            }
-            if (more && ++ks == KST) {
-              ks = 0;
-              k_phase ^= 1;
+            if (u == 1) {
+              umma_commit(v_empty + vs);
+              if (++vs == VST) {
+                vs = 0;
+                v_phase ^= 1;
+              }
+              if (ahead) {
+                umma_commit(k_empty + ks);
+                if (++ks == KST) {
+                  ks = 0;
+                  k_phase ^= 1;
+                }
+              }
             }
           }
         }
+        PROF_ADD(tot, prof_start);
+        PROF_FLUSH(0, tot); PROF_FLUSH(1, wp); PROF_FLUSH(2, wk); PROF_FLUSH(3, wv); PROF_FLUSH(4, wq);
+        PROF_FLUSH(5, wo); PROF_FLUSH(6, nt);
       }
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SOFT_REGS));
     // ======================= softmax / correction / epilogue (one warpgroup per half) =======================
-    const int hf = (warp - NWARP_CTRL) / 4;          // half of the item this warpgroup owns
+    const int hf = (warp - NWARP_CTRL) / 4;                 // half of the item this warpgroup owns
     const int row = (threadIdx.x - 32 * NWARP_CTRL) % 128;  // TMEM lane == row of the half
     const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
     const uint32_t tS = tmem + 128 * hf + lane_off;
     const uint32_t tO = tmem + 256 + 128 * hf + lane_off;
-    int stage = 0;  // K ring stage (key coordinates)
-    uint32_t kv_phase = 0, s_phase = 0, o_phase = 0;
+    int kps = 0;  // key-coordinate ring
+    uint32_t kp_phase = 0, o_phase = 0;
+    uint32_t s_phase[2] = {0, 0};
+    uint32_t n_sub = 0;  // sub-tiles this half has processed (= P V commits on pv_done[hf])
     const int G = P.H / P.Hkv;
+    PROF_DECL(stot); PROF_DECL(sws); PROF_DECL(sld); PROF_DECL(smask); PROF_DECL(ssm); PROF_DECL(sresc);
+    PROF_DECL(spst); PROF_DECL(sepi); PROF_DECL(snt); PROF_DECL(snr); PROF_DECL(sfetch); PROF_DECL(sitem);
+    [[maybe_unused]] const long long sprof_start = PROF_T();
     for (int i = 0;; ++i) {
+      long long t0 = PROF_T();
       const int idx = fetch(i);
+      PROF_ADD(sfetch, t0);
       __syncwarp();
       if (lane == 0) mbar_arrive(sched_empty + i % SCHED_RING);
       if (idx < 0) break;
@@ -450,18 +530,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (it.n_tiles <= 0) continue;  // empty slot: nothing to compute or write
       if (hf == 1 && !it.has_b) {
         // absent half: only release the key-coordinate stages
+        SegIter si;
+        si.init(P, it);
         for (int t = 0; t < it.n_tiles; ++t) {
-          mbar_wait(k_full + stage, kv_phase);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(k_empty + stage);
-          if (++stage == KST) {
-            stage = 0;
-            kv_phase ^= 1;
+          const TileInfo e = si.next(P, it);
+          if (e.space && (e.pred || P.fingerprint)) {
+            mbar_wait(kp_full + kps, kp_phase);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(kp_empty + kps);
+            if (++kps == NKP) {
+              kps = 0;
+              kp_phase ^= 1;
+            }
           }
         }
         continue;
       }
       if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 3] = gtimer();
+      t0 = PROF_T();
       // row identity
       const int qrow = it.q_row0 + hf * BLK + row;
       int xpos, xrank;
@@ -484,25 +570,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int kv = it.head / G;
       SegIter si;
       si.init(P, it);
+      PROF_ADD(sitem, t0);
       for (int t = 0; t < it.n_tiles; ++t) {
         const TileInfo e = si.next(P, it);
         const uint32_t space = e.space, pred = e.pred, role = e.role, rmode = e.rmode, inst = e.inst;
-        mbar_wait(s_full + hf, s_phase);
-        s_phase ^= 1;
-        tc_fence_after();
-        float s[BLK];
-#pragma unroll
-        for (int c = 0; c < BLK / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tS + c * 32, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(r[j]);  // raw scores
-        }
-        if (pred || (P.fingerprint && space)) mbar_wait(k_full + stage, kv_phase);
-        if (pred || P.fingerprint) {
-          // admitted-key bit mask of this tile (bit c <-> key c), then one unrolled select
-          uint32_t mw[4] = {0u, 0u, 0u, 0u};
+        const bool masked = pred || P.fingerprint;
+        uint32_t mw[4] = {0u, 0u, 0u, 0u};  // admitted-key mask of the tile (bit c <-> key c)
+        if (masked) {
+          const bool need_kp = space;
+          if (need_kp) mbar_wait(kp_full + kps, kp_phase);
+          const int* kp = kpos_s + kps * BLK;
           if (valid) {
             const int kbase = e.krow - kv * P.S;
             if (!pred) {
@@ -528,8 +605,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 n_lt_local = min(max(x - local - kbase + 1, 0), BLK);  // keys with y <= x - local
                 ybase = kbase;
               } else {
-                const int* kp = kpos_s + stage * BLK;
-                const int* yc = rmode ? (krank_s + stage * BLK) : kp;
+                const int* yc = rmode ? (krank_s + kps * BLK) : kp;
                 n_causal = count_le(kp, xpos);
                 n_sink = (role == R_A || role == R_NOTA) ? count_le(yc, sink - 1) : 0;
                 n_lt_local = (role == R_A || role == R_NOTA) ? count_le(yc, x - local) : 0;
@@ -560,7 +636,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 while (bitsw) {
                   const int c = w * 32 + __ffs(bitsw) - 1;
                   bitsw &= bitsw - 1;
-                  const long long ypos = space ? kpos_s[stage * BLK + c] : kbase + c;
+                  const long long ypos = space ? kp[c] : kbase + c;
                   fp_cnt += 1;
                   fp_s1 += ypos;
                   fp_s2 += ypos * ypos;
@@ -568,63 +644,128 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
           }
-#pragma unroll
-          for (int c = 0; c < BLK; ++c)
-            if (!((mw[c >> 5] >> (c & 31)) & 1u)) s[c] = -INFINITY;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(k_empty + stage);  // key coordinates of this stage consumed
-        if (++stage == KST) {
-          stage = 0;
-          kv_phase ^= 1;
-        }
-        // ---- online softmax (log2 domain), lazy rescale ----
-        float mt = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < BLK; ++c) mt = fmaxf(mt, s[c]);
-        if (mt > -INFINITY) mt *= P.scale_log2;  // tau * log2(e) > 0 commutes with max
-        float alpha = 1.f;
-        bool rescale = false;
-        if (mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt > -INFINITY)) {
-          alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt);
-          rescale = (m_used != -INFINITY);
-          m_used = mt;
-        }
-        const float mu = (m_used == -INFINITY) ? 0.f : m_used;
-        float ls = 0.f;
-        uint32_t pk[BLK / 2];
-#pragma unroll
-        for (int c = 0; c < BLK; c += 2) {
-          const float p0 = ex2(fmaf(s[c], P.scale_log2, -mu));
-          const float p1 = ex2(fmaf(s[c + 1], P.scale_log2, -mu));
-          ls += p0 + p1;
-          pk[c / 2] = pack_bf16(p0, p1);
-        }
-        l_sum = l_sum * alpha + ls;
-        // O correction only when the running max moved; O_h is quiescent: P V_h(t-1) was
-        // issued before S_h(t), which has completed.
-        if (t > 0 && __any_sync(0xffffffffu, rescale)) {
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + c * 32, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
-            tmem_st32(tO + c * 32, r);
+          if (need_kp) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(kp_empty + kps);  // key coordinates of this stage consumed
+            if (++kps == NKP) {
+              kps = 0;
+              kp_phase ^= 1;
+            }
           }
         }
-        // P (bf16 pairs) -> TMEM columns [0, 64) of this half's S buffer
-        tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(p_full + hf);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          t0 = PROF_T();
+          mbar_wait(s_full + 2 * hf + u, s_phase[u]);
+          PROF_ADD(sws, t0);
+          t0 = PROF_T();
+          s_phase[u] ^= 1;
+          tc_fence_after();
+#ifdef MMI_NOSOFT
+          // pipeline ceiling experiment (scratch builds only): no softmax work at all
+          tc_fence_before();
+          mbar_arrive(p_full + 2 * hf + u);
+          ++n_sub;
+          continue;
+#endif
+          float s[64];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tS + 64 * u + c * 32, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(r[j]);  // raw scores
+          }
+          PROF_ADD(sld, t0);
+          t0 = PROF_T();
+          if (masked) {
+#pragma unroll
+            for (int c = 0; c < 64; ++c)
+              if (!((mw[2 * u + (c >> 5)] >> (c & 31)) & 1u)) s[c] = -INFINITY;
+          }
+          PROF_ADD(smask, t0);
+          t0 = PROF_T();
+          // ---- online softmax (log2 domain), lazy rescale ----
+          float mx[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mx[j] = fmaxf(s[j], s[j + 8]);
+#pragma unroll
+          for (int c = 16; c < 64; c += 16)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mx[j] = fmaxf(mx[j], fmaxf(s[c + j], s[c + 8 + j]));
+          float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+          if (mt > -INFINITY) mt *= P.scale_log2;  // tau * log2(e) > 0 commutes with max
+          float alpha = 1.f;
+          bool rescale = false;
+          if (mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt > -INFINITY)) {
+            alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt);
+            rescale = (m_used != -INFINITY);
+            m_used = mt;
+          }
+          const float mu = (m_used == -INFINITY) ? 0.f : m_used;
+          const float2 sc2 = make_float2(P.scale_log2, P.scale_log2), nmu2 = make_float2(-mu, -mu);
+          float2 ls2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                           make_float2(0.f, 0.f)};
+          uint32_t pk[32];
+#pragma unroll
+          for (int c = 0; c < 64; c += 2) {
+            const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nmu2);
+            float2 pr;
+            if ((EMU_MASK >> ((c / 2) % 8)) & 1u) {
+              pr = exp2_poly2(x);
+            } else {
+              pr.x = ex2(x.x);
+              pr.y = ex2(x.y);
+            }
+            ls2[(c / 2) % 4] = fadd2(ls2[(c / 2) % 4], pr);
+            pk[c / 2] = pack_bf16(pr.x, pr.y);
+          }
+          const float2 lsa = fadd2(fadd2(ls2[0], ls2[1]), fadd2(ls2[2], ls2[3]));
+          l_sum = l_sum * alpha + (lsa.x + lsa.y);
+          PROF_ADD(ssm, t0);
+          t0 = PROF_T();
+          // O correction only when the running max moved (rare).  P V of the previous sub-tile
+          // may still be in flight (S of this sub-tile was issued before it): wait for it.
+          if (__any_sync(0xffffffffu, rescale)) {
+            mbar_wait(pv_done + hf, (n_sub - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t r[32];
+              tmem_ld32(tO + c * 32, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
+              tmem_st32(tO + c * 32, r);
+            }
+#ifdef MMI_PROF
+            prof_snr += 1;
+#endif
+          }
+          PROF_ADD(sresc, t0);
+          t0 = PROF_T();
+          // P (bf16 pairs) -> TMEM columns [64u, 64u + 32) of this half's S buffer
+          tmem_st32(tS + 64 * u, pk);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(p_full + 2 * hf + u);
+          ++n_sub;
+          PROF_ADD(spst, t0);
+#ifdef MMI_PROF
+          prof_snt += 1;
+#endif
+        }
       }
+      t0 = PROF_T();
       // ---- epilogue ----
       mbar_wait(o_full + hf, o_phase);
       o_phase ^= 1;
       tc_fence_after();
+      // no admitted key in this item <=> the running max never left -inf (the polynomial exp2
+      // maps masked scores to 2^-125, so l_sum alone does not tell)
+      if (m_used == -INFINITY) l_sum = 0.f;
       const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
       const float lse_v = l_sum > 0.f ? (m_used + __log2f(l_sum)) * 0.6931471805599453f : -INFINITY;
       if (P.fingerprint) {
@@ -683,6 +824,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         P.part_lse[it.out_row0 + hf * BLK + row] = valid ? lse_v : -INFINITY;
       }
       if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 6] = gtimer();
+      PROF_ADD(sepi, t0);
+    }
+    PROF_ADD(stot, sprof_start);
+    if (lane == 0) {
+      PROF_FLUSH(8, stot); PROF_FLUSH(9, sws); PROF_FLUSH(10, sld); PROF_FLUSH(11, smask); PROF_FLUSH(12, ssm);
+      PROF_FLUSH(13, sresc); PROF_FLUSH(14, spst); PROF_FLUSH(15, sepi); PROF_FLUSH(16, snt); PROF_FLUSH(17, snr);
+      PROF_FLUSH(18, sfetch); PROF_FLUSH(19, sitem);
     }
   }
   tc_fence_before();
@@ -694,6 +842,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // ------------------------------------------------------------------ host side
+#ifdef MMI_PROF
+extern "C" __attribute__((visibility("default"))) int mmi_debug_prof(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_prof, sizeof(g_prof));
+  if (reset) {
+    unsigned long long z[32] = {0};
+    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
