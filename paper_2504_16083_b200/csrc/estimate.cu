@@ -565,13 +565,14 @@ __global__ void __launch_bounds__(256) grid_acc_kernel(const DInst* __restrict__
   for (int q = 0; q < ns; ++q) {
     const int s = s0 + q;
     unsigned long long* gs = g + (size_t)(s - x.smin) * x.smax;
+    const int r = j_begin % s;  // local index i has residue (r + i) mod s
     if (s <= 256) {
       const int G = 256 / s;
       unsigned long long sum = 0;
       if (tid < G * s) {
-        const int grp = tid / s, p = tid % s;
+        const int grp = tid / s, p = tid - grp * s;
         // first local index with (j_begin + i) = p (mod s)
-        const int i0 = (((p - j_begin) % s) + s) % s;
+        const int i0 = p >= r ? p - r : p - r + s;
         for (int i = i0 + grp * s; i < len; i += G * s) sum += chunk[i];
       }
       part[tid] = sum;
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(256) grid_acc_kernel(const DInst* __restrict__
       __syncthreads();
     } else {
       for (int p = tid; p < s; p += blockDim.x) {
-        const int i0 = (((p - j_begin) % s) + s) % s;
+        const int i0 = p >= r ? p - r : p - r + s;
         unsigned long long sum = 0;
         for (int i = i0; i < len; i += s) sum += chunk[i];
         if (sum) atomicAdd(&gs[p], sum);
