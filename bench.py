@@ -173,7 +173,7 @@ def main():
         d = gen_qkv(wl, seed=args.seed)
         vals, walls = [], []
         for step in range(args.warmup + args.steps):
-            ms, wall, cores, sample = oracle_sample(wl, d, seed=step)
+            ms, wall, cores, sample = oracle_sample(wl, d, seed=step, n_rows=1024)
             if step >= args.warmup:
                 vals.append(ms)
                 walls.append(wall)
@@ -327,7 +327,7 @@ def main():
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
-        ms_cpu, wall, cores, sample = oracle_sample(wl, d)
+        ms_cpu, wall, cores, sample = oracle_sample(wl, d, n_rows=1536)
         cpu = {"value": ms_cpu, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                "sample_wall_s": wall}
 

@@ -51,6 +51,8 @@ struct Cfg {
   static constexpr int VST = (D == 128) ? 2 : 3;  // V ring stages
 };
 constexpr int SCHED_RING = 4;
+constexpr int SCHED_ENTRY = 128;  // bytes per ring entry: item index + staged WorkItem
+static_assert(16 + sizeof(WorkItem) <= SCHED_ENTRY, "WorkItem does not fit the scheduler ring entry");
 constexpr int NWARP_CTRL = 4;                      // scheduler+Q, MMA, K loader, V loader
 constexpr int NWARP_SOFT = 8;                      // 2 softmax warpgroups: one per query half
 constexpr int NTHREADS = 32 * (NWARP_CTRL + NWARP_SOFT);
@@ -89,11 +91,12 @@ struct Smem {
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
   static constexpr int OFF_KPOS = OFF_V + VST * KV_BYTES;
   static constexpr int OFF_KRANK = OFF_KPOS + NKP * BLK * 4;
-  static constexpr int OFF_SCHED = OFF_KRANK + NKP * BLK * 4;
-  static constexpr int OFF_BAR = OFF_SCHED + 64;
+  static constexpr int OFF_SCHED = OFF_KRANK + NKP * BLK * 4;  // [SCHED_RING] x {idx, pad, WorkItem}: 128 B
+  static constexpr int OFF_RI = OFF_SCHED + SCHED_RING * SCHED_ENTRY;     // [2] x {pos[256], rank[256]} of the item's rows
+  static constexpr int OFF_BAR = OFF_RI + 2 * 2 * 2 * BLK * 4;
   // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2][2] p_full[2][2] o_full[2]
   // o_empty[2] pv_done[2] sched_full[R] sched_empty[R] kp_full[NKP] kp_empty[NKP]
-  static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 14 + 2 * SCHED_RING + 2 * NKP;
+  static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 14 + 2 * SCHED_RING + 2 * NKP + 4;
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
   static constexpr int TOTAL = OFF_TMEM + 16;
   static constexpr int ALLOC = TOTAL + 1024;  // alignment slack
@@ -104,7 +107,7 @@ struct ItemView {
       row_mod, rb, has_b;
 };
 
-__device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx) {
+__device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx, const WorkItem* staged) {
   ItemView v;
   if (P.dense) {
     const int nb = (P.S + BLK - 1) / BLK;
@@ -127,7 +130,7 @@ __device__ __forceinline__ ItemView load_item(const AttnParams& P, int idx) {
     v.row_mod = -1;
     return v;
   }
-  const WorkItem w = P.items[idx];
+  const WorkItem w = *staged;  // copied to shared memory by the scheduler
   v.head = w.head;
   v.q_row0 = w.q_row0;
   v.seg_off = w.seg_off;
@@ -248,11 +251,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* sched_full = pv_done + 2;
   uint64_t* sched_empty = sched_full + SCHED_RING;
   uint64_t* kp_full = sched_empty + SCHED_RING;
+  uint64_t* ri_full = kp_full + 2 * NKP;  // [2] row identities (positions / ranks) of an item staged
+  uint64_t* ri_empty = ri_full + 2;     // [2]
   uint64_t* kp_empty = kp_full + NKP;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
   int32_t* kpos_s = reinterpret_cast<int32_t*>(smem + L::OFF_KPOS);
   int32_t* krank_s = reinterpret_cast<int32_t*>(smem + L::OFF_KRANK);
-  volatile int32_t* sched_ring = reinterpret_cast<volatile int32_t*>(smem + L::OFF_SCHED);
+  volatile int32_t* sched_ring = reinterpret_cast<volatile int32_t*>(smem + L::OFF_SCHED);  // stride SCHED_ENTRY
+  int32_t* ri_s = reinterpret_cast<int32_t*>(smem + L::OFF_RI);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -285,6 +291,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(kp_full + i, 1);
       mbar_init(kp_empty + i, NWARP_SOFT);  // one arrival per softmax warp
     }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(ri_full + i, 1);
+      mbar_init(ri_empty + i, NWARP_SOFT);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_holder);
@@ -305,7 +315,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   auto fetch = [&](int i) -> int {
     const int slot = i % SCHED_RING;
     mbar_wait(sched_full + slot, (i / SCHED_RING) & 1);
-    return sched_ring[slot];
+    return sched_ring[slot * (SCHED_ENTRY / 4)];
+  };
+  // the item of ring entry i (the scheduler staged its WorkItem next to the index)
+  auto item_of = [&](int i, int idx) -> ItemView {
+    return load_item(P, idx, reinterpret_cast<const WorkItem*>(smem + L::OFF_SCHED + (i % SCHED_RING) * SCHED_ENTRY + 16));
   };
 
   if (warp < NWARP_CTRL) {
@@ -313,18 +327,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp == 0) {
       // ======================= scheduler + Q loader =======================
       if (elect_one()) {
-        uint32_t q_phase = 0;
+        uint32_t q_phase = 0, rs_phase = 0;
+        int rs = 0;
         for (int i = 0;; ++i) {
           const int slot = i % SCHED_RING;
           mbar_wait(sched_empty + slot, ((i / SCHED_RING) & 1) ^ 1);
           int idx = (i == 0) ? (int)blockIdx.x : (int)gridDim.x + (int)atomicAdd(P.sched, 1u);
           if (idx >= n_items) idx = -1;
-          sched_ring[slot] = idx;
+          sched_ring[slot * (SCHED_ENTRY / 4)] = idx;
+          if (idx >= 0 && !P.dense) {
+            const int4* src = reinterpret_cast<const int4*>(P.items + idx);
+            int4* dst = reinterpret_cast<int4*>(smem + L::OFF_SCHED + slot * SCHED_ENTRY + 16);
+#pragma unroll
+            for (int w = 0; w < (int)(sizeof(WorkItem) / 16); ++w) dst[w] = src[w];
+          }
           mbar_arrive(sched_full + slot);
           if (idx < 0) break;
-          const ItemView it = load_item(P, idx);
+          const ItemView it = item_of(i, idx);
           if (it.n_tiles <= 0) continue;
           if (P.dbg) P.dbg[idx * 8 + 0] = gtimer();
+          if (!P.dense) {
+            // stage the rows' positions / ranks (contiguous slices) for the softmax warps
+            mbar_wait(ri_empty + rs, rs_phase ^ 1);
+            const int nrows = it.has_b ? 2 * BLK : BLK;
+            int32_t* rip = ri_s + rs * 4 * BLK;
+            if (it.q_gathered) {
+              mbar_arrive_expect_tx(ri_full + rs, 2 * nrows * 4);
+              bulk_load(rip, P.qg_pos + it.q_row0, nrows * 4, ri_full + rs);
+              bulk_load(rip + 2 * BLK, P.qg_rank + it.q_row0, nrows * 4, ri_full + rs);
+            } else {
+              const int x0 = it.q_row0 - it.head * P.S;
+              const int n4 = P.rank ? (min(nrows, P.S - x0) & ~3) : 0;  // whole 16-byte groups
+              mbar_arrive_expect_tx(ri_full + rs, n4 * 4);
+              if (n4 > 0) bulk_load(rip + 2 * BLK, P.rank + x0, n4 * 4, ri_full + rs);
+            }
+            if (++rs == 2) {
+              rs = 0;
+              rs_phase ^= 1;
+            }
+          }
           mbar_wait(q_empty, q_phase ^ 1);
           q_phase ^= 1;
           mbar_arrive_expect_tx(q_full, (it.has_b ? 2 : 1) * L::Q_BYTES);
@@ -350,7 +391,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int idx = fetch(i);
           mbar_arrive(sched_empty + i % SCHED_RING);
           if (idx < 0) break;
-          const ItemView it = load_item(P, idx);
+          const ItemView it = item_of(i, idx);
           if (it.n_tiles <= 0) continue;
           SegIter si;
           si.init(P, it);
@@ -403,7 +444,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int idx = fetch(i);
           mbar_arrive(sched_empty + i % SCHED_RING);
           if (idx < 0) break;
-          const ItemView it = load_item(P, idx);
+          const ItemView it = item_of(i, idx);
           const int n = it.n_tiles;
           if (n <= 0) continue;
           const int nh = it.has_b ? 2 : 1;
@@ -514,6 +555,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int kps = 0;  // key-coordinate ring
     uint32_t kp_phase = 0, o_phase = 0;
     uint32_t s_phase[2] = {0, 0};
+    int rs = 0;  // row-identity stage
+    uint32_t rs_phase = 0;
     uint32_t n_sub = 0;  // sub-tiles this half has processed (= P V commits on pv_done[hf])
     const int G = P.H / P.Hkv;
     PROF_DECL(stot); PROF_DECL(sws); PROF_DECL(sld); PROF_DECL(smask); PROF_DECL(ssm); PROF_DECL(sresc);
@@ -526,8 +569,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(sched_empty + i % SCHED_RING);
       if (idx < 0) break;
-      const ItemView it = load_item(P, idx);
+      const ItemView it = item_of(i, idx);
       if (it.n_tiles <= 0) continue;  // empty slot: nothing to compute or write
+      // row identity (positions / ranks staged in shared memory by warp 0)
+      int xpos = it.q_row0 + hf * BLK + row - it.head * P.S, xrank = xpos;
+      if (!P.dense) {
+        mbar_wait(ri_full + rs, rs_phase);
+        const int32_t* rip = ri_s + rs * 4 * BLK;
+        const int li = hf * BLK + row;
+        if (it.q_gathered) {
+          xpos = rip[li];
+          xrank = rip[2 * BLK + li];
+        } else if (P.rank) {
+          const int x0 = it.q_row0 - it.head * P.S;
+          const int n4 = min((it.has_b ? 2 : 1) * BLK, P.S - x0) & ~3;
+          xrank = li < n4 ? rip[2 * BLK + li] : (xpos < P.S ? P.rank[xpos] : xpos);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ri_empty + rs);
+        if (++rs == 2) {
+          rs = 0;
+          rs_phase ^= 1;
+        }
+      }
       if (hf == 1 && !it.has_b) {
         // absent half: only release the key-coordinate stages
         SegIter si;
@@ -548,16 +612,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 3] = gtimer();
       t0 = PROF_T();
-      // row identity
-      const int qrow = it.q_row0 + hf * BLK + row;
-      int xpos, xrank;
-      if (it.q_gathered) {
-        xpos = P.qg_pos[qrow];
-        xrank = P.qg_rank[qrow];
-      } else {
-        xpos = qrow - it.head * P.S;
-        xrank = (xpos < P.S && P.rank) ? P.rank[xpos] : xpos;
-      }
       bool valid = xpos >= 0 && xpos < P.S;
       if (valid && it.row_mod >= 0) valid = (P.labels[xpos] == it.row_mod);
       bool write = valid;
