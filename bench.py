@@ -238,6 +238,7 @@ def main():
         step(False)
     torch.cuda.synchronize()
     tiles = sp.total_tiles()           # computed key tiles of this rank's index (outside the timed region)
+    moved = mmi.mmi_traffic_stats(lpb, lheads, sp.ws)  # rows the permute step moves (outside the timed region)
     if dist: dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -277,6 +278,27 @@ def main():
             "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)", "kernel": "mmi::attn_kernel<%d>" % pb.head_dim, "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"
             if "_fallback" not in peaks else "fallback 1.59 PF", "tiles": int(tiles),
             "flops_per_tile": flops_tile}
+
+    # memory-bound stages: algorithmic bytes per step / stage event time, vs the measured HBM peak
+    st = mmi.mmi_plan_stats(lpb, lheads)
+    D, S_ = pb.head_dim, pb.seq_len
+    nkv = kv1 - kv0
+    hbm_peak = float(peaks["hbm_gbs"])
+    alg = {
+        # gathered Q-bar / K-bar / V-bar rows: read + write, bf16
+        "permute": ((moved["qg_read"] + moved["qg_written"] + 2 * (moved["kg_read"] + moved["kg_written"])) * D * 2,
+                    "(rows read + rows written) of Qbar, Kbar, Vbar x D x 2 B (mmi_traffic_stats)"),
+        # LSE merge: two fp32 partial rows + LSEs in, one bf16 row out, per token of a merged head
+        "unpermute": (st["merge_heads"] * S_ * (2 * D * 4 + 2 * 4 + D * 2),
+                      "merged heads x S x (2 fp32 partial rows + 2 LSE + 1 bf16 row)"),
+        # slab estimation: K streamed once per pass (2 passes) + column masses written per slab
+        "estimate": (2 * nkv * S_ * D * 2 + st["slabs"] * S_ * 4,
+                     "2 passes x K [Hkv,S,D] bf16 + slabs x S x 4 B column masses"),
+    }
+    hbm = {"peak_GBs": hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs", "stages": {}}
+    for name, (nbytes, how) in alg.items():
+        gbs = nbytes / (stage[name] * 1e-3) / 1e9 if stage[name] > 0 else None
+        hbm["stages"][name] = {"bytes": int(nbytes), "GBps": gbs, "frac": (gbs / hbm_peak) if gbs else None, "bytes_def": how}
 
     # same-build dense comparator (a separate measurement, not in the timed steps)
     dense_ms = None
@@ -345,7 +367,7 @@ def main():
             "dense_ms": dense_ms,
             "speedup_vs_dense": (dense_ms / ms) if dense_ms else None,
             "tile_density": tiles / dense_tiles,
-            "roofline": roof,
+            "roofline": roof, "hbm": hbm,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": count_launches(lheads),

@@ -130,6 +130,20 @@ MMI_API mmi_status mmi_unpermute(const mmi_problem* problem, const mmi_head_conf
 MMI_API mmi_status mmi_dense_prefill(const mmi_problem* problem, const void* q, const void* k, const void* v, void* o,
                              float* lse, mmi_stream_t stream);
 
+/* Sizes of the plan for (problem, cfg_host), host-only (no device work), for
+ * reporting algorithmic traffic: out[0] = gathered Q rows (Q̄), out[1] = gathered
+ * K/V rows (K̄ and V̄ each), out[2] = heads with LSE-merged rows, out[3] = estimation
+ * slabs, out[4] = partial-output rows.  Writes min(n, 5) values.  Returns
+ * MMI_E_INVALID / MMI_E_SHAPE / MMI_E_CONFIG like mmi_workspace_bytes' validation. */
+MMI_API mmi_status mmi_plan_stats(const mmi_problem* problem, const mmi_head_config* cfg_host, int64_t* out_host,
+                                  int n);
+
+/* REPORTING ONLY (synchronises the stream; call after mmi_estimate_index).  Rows the
+ * permute step actually moves: out[0] / out[1] = Q̄ rows read / written, out[2] /
+ * out[3] = K̄ (and V̄) rows read / written (padding rows are written as zeros). */
+MMI_API mmi_status mmi_traffic_stats(const mmi_problem* problem, const mmi_head_config* cfg_host, const void* ws,
+                                     size_t ws_bytes, int64_t* out_host, mmi_stream_t stream);
+
 /* TEST ONLY (synchronises the stream).  Copies the estimated index of head h
  * to host_buf as int32 words: see mmi_export_layout in the Python binding.
  * Returns the number of int32 words needed when host_buf is NULL (via *words). */

@@ -133,6 +133,17 @@ extern "C" size_t mmi_workspace_bytes(const mmi_problem* pb, const mmi_head_conf
   return P.total;
 }
 
+extern "C" mmi_status mmi_plan_stats(const mmi_problem* pb, const mmi_head_config* cfg, int64_t* out, int n) {
+  if (!out || n < 0) return fail(MMI_E_INVALID, "null output");
+  Plan P;
+  const mmi_status st = prepare(pb, cfg, nullptr, 0, P, false);
+  if (st != MMI_OK) return st;
+  const int64_t v[5] = {P.qg_rows, P.kg_rows, (int64_t)P.merge_heads.size(), (int64_t)P.slabs.size(),
+                        (int64_t)P.part_rows};
+  for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
+  return MMI_OK;
+}
+
 extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_config* cfg, const void* q,
                                          const void* k, const uint8_t* modality, void* ws, size_t ws_bytes,
                                          mmi_stream_t stream) {
@@ -337,6 +348,30 @@ extern "C" mmi_status mmi_dense_prefill(const mmi_problem* pb, const void* q, co
 //   [0] n_inst
 //   per instance: kind, qa, kb, rank, s, p, valid, J (2 words, double bits), nV, nS, V[nV], Sl[nS]
 //   then: items with tiles, total tiles (2 words, int64), segments
+extern "C" mmi_status mmi_traffic_stats(const mmi_problem* pb, const mmi_head_config* cfg, const void* ws,
+                                        size_t ws_bytes, int64_t* out, mmi_stream_t stream) {
+  Plan P;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  if (st != MMI_OK) return st;
+  if (!out) return fail(MMI_E_INVALID, "null output");
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  void* w = const_cast<void*>(ws);
+  auto count = [&](const Region& r, int64_t rows, int64_t& rd, int64_t& wr) -> bool {
+    rd = wr = 0;
+    if (rows <= 0) return true;
+    std::vector<int> src(rows);
+    if (cudaMemcpy(src.data(), at<int>(w, r), sizeof(int) * rows, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    for (int v : src) {
+      rd += v >= 0;
+      wr += v >= -1;  // -1: padding row written as zeros, -2: never touched
+    }
+    return true;
+  };
+  if (!count(P.qg_src, P.qg_rows, out[0], out[1]) || !count(P.kg_src, P.kg_rows, out[2], out[3]))
+    return fail(MMI_E_CUDA, "copy of the gather sources failed");
+  return MMI_OK;
+}
+
 extern "C" mmi_status mmi_export_index(const mmi_problem* pb, const mmi_head_config* cfg, const void* ws,
                                        size_t ws_bytes, int32_t head, int32_t* host_buf, size_t* words,
                                        mmi_stream_t stream) {

@@ -705,58 +705,95 @@ __global__ void gather_rows_kernel(const int* __restrict__ src, int64_t rows, co
 }
 
 // ================================================================ merge (a8)
+// One warp merges MERGE_R rows: lanes 0..R-1 resolve the rows' metadata (a chain of
+// dependent loads: modality position, instance, grid result, residue-class offset) in
+// parallel, then all partial-row loads of the R rows are issued before any use.
+constexpr int MERGE_R = 4;
 __global__ void merge_kernel(IndexCtx C, int D, const int* __restrict__ heads_list, int n_rows,
                              __nv_bfloat16* __restrict__ o, float* __restrict__ lse) {
   const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
-  if (warp_g >= n_rows) return;
+  const int i_base = warp_g * MERGE_R;
+  if (i_base >= n_rows) return;
   const int h = heads_list[blockIdx.y];
   const DHead hd = C.heads[h];
-  const int i = warp_g;
-  int pos, grp;
-  if (hd.qmod_view < 0) {
-    pos = i;
-    if (pos >= C.S) return;
-    grp = 0;
-  } else {
-    if (i >= C.info[MI_PADOFF + MAX_MOD]) return;
-    pos = C.modpos[i];
-    if (pos < 0) return;
-    grp = C.labels[pos];
-  }
-  const int gi = hd.sl_inst[grp];
-  if (gi < 0) return;
-  const DInst x = C.insts[h * MAX_INST + gi];
-  const GridRes g = C.gridres[x.grid_id];
-  const int coord = x.rank ? C.rank[pos] : pos;
-  const int r = coord % g.s;
-  if ((x.flags & GF_H) && r == g.p) return;  // written by the HROW pass
-  const float* o0 = C.part_o + (size_t)(hd.part_rows0 + i) * D;
-  float l0 = C.part_lse[hd.part_rows0 + i];
-  float l1 = -INFINITY;
-  const float* o1 = nullptr;
-  if (!(r == g.p && (x.flags & (GF_H | GF_V)))) {
-    ClassGeo cg;
-    cg.init(x.rank ? C.info[MI_CNT + x.qa] : C.S, g.s);
-    const int j = x.pad[0] + cg.classoff(r) + coord / g.s;
-    o1 = C.part_o + (size_t)j * D;
-    l1 = C.part_lse[j];
-  }
-  const float m = fmaxf(l0, l1);
-  const float w0 = (l0 == -INFINITY) ? 0.f : __expf(l0 - m);
-  const float w1 = (l1 == -INFINITY) ? 0.f : __expf(l1 - m);
-  const float tot = w0 + w1;
-  const float inv = tot > 0.f ? 1.f / tot : 0.f;
-  __nv_bfloat16* orow = o + ((size_t)h * C.S + pos) * D;
-  for (int d = lane * 2; d < D; d += 64) {
-    float a0 = o0[d] * w0, a1 = o0[d + 1] * w0;
-    if (o1) {
-      a0 += o1[d] * w1;
-      a1 += o1[d + 1] * w1;
+  int pos = -1;
+  long long j0 = -1, j1 = -1;
+  float w0 = 0.f, w1 = 0.f, inv = 0.f, lsev = -INFINITY;
+  if (lane < MERGE_R && i_base + lane < n_rows) {
+    const int i = i_base + lane;
+    int grp = 0;
+    bool ok = true;
+    if (hd.qmod_view < 0) {
+      pos = i;
+      ok = pos < C.S;
+    } else {
+      ok = i < C.info[MI_PADOFF + MAX_MOD];
+      pos = ok ? C.modpos[i] : -1;
+      ok = ok && pos >= 0;
+      if (ok) grp = C.labels[pos];
     }
-    *reinterpret_cast<__nv_bfloat162*>(orow + d) = __floats2bfloat162_rn(a0 * inv, a1 * inv);
+    const int gi = ok ? hd.sl_inst[grp] : -1;
+    if (gi >= 0) {
+      const DInst x = C.insts[h * MAX_INST + gi];
+      const GridRes g = C.gridres[x.grid_id];
+      const int coord = x.rank ? C.rank[pos] : pos;
+      const int r = coord % g.s;
+      if ((x.flags & GF_H) && r == g.p) {
+        pos = -1;  // written by the HROW pass
+      } else {
+        j0 = hd.part_rows0 + i;
+        const float l0 = C.part_lse[j0];
+        float l1 = -INFINITY;
+        if (!(r == g.p && (x.flags & (GF_H | GF_V)))) {
+          ClassGeo cg;
+          cg.init(x.rank ? C.info[MI_CNT + x.qa] : C.S, g.s);
+          j1 = x.pad[0] + cg.classoff(r) + coord / g.s;
+          l1 = C.part_lse[j1];
+        }
+        const float m = fmaxf(l0, l1);
+        w0 = (l0 == -INFINITY) ? 0.f : __expf(l0 - m);
+        w1 = (l1 == -INFINITY) ? 0.f : __expf(l1 - m);
+        const float tot = w0 + w1;
+        inv = tot > 0.f ? 1.f / tot : 0.f;
+        lsev = tot > 0.f ? m + __logf(tot) : -INFINITY;
+      }
+    } else {
+      pos = -1;
+    }
   }
-  if (lane == 0 && lse) lse[(size_t)h * C.S + pos] = tot > 0.f ? m + __logf(tot) : -INFINITY;
+  constexpr int NC = 2;  // 64-column chunks per row at D = 128 (1 used at D = 64); a float2 per lane each
+  float2 a[MERGE_R][NC], b[MERGE_R][NC];
+  const int nc = D / 64;
+#pragma unroll
+  for (int r = 0; r < MERGE_R; ++r) {
+    const int p = __shfl_sync(0xffffffffu, pos, r);
+    const long long q0 = __shfl_sync(0xffffffffu, j0, r), q1 = __shfl_sync(0xffffffffu, j1, r);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      a[r][c] = make_float2(0.f, 0.f);
+      b[r][c] = make_float2(0.f, 0.f);
+      if (c < nc && p >= 0) {
+        a[r][c] = *reinterpret_cast<const float2*>(C.part_o + q0 * D + c * 64 + 2 * lane);
+        if (q1 >= 0) b[r][c] = *reinterpret_cast<const float2*>(C.part_o + q1 * D + c * 64 + 2 * lane);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < MERGE_R; ++r) {
+    const int p = __shfl_sync(0xffffffffu, pos, r);
+    if (p < 0) continue;
+    const float x0 = __shfl_sync(0xffffffffu, w0, r), x1 = __shfl_sync(0xffffffffu, w1, r);
+    const float xi = __shfl_sync(0xffffffffu, inv, r);
+    __nv_bfloat16* orow = o + ((size_t)h * C.S + p) * D;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      if (c >= nc) break;
+      const float v0 = (a[r][c].x * x0 + b[r][c].x * x1) * xi, v1 = (a[r][c].y * x0 + b[r][c].y * x1) * xi;
+      *reinterpret_cast<__nv_bfloat162*>(orow + c * 64 + 2 * lane) = __floats2bfloat162_rn(v0, v1);
+    }
+  }
+  if (lane < MERGE_R && pos >= 0 && lse) lse[(size_t)h * C.S + pos] = lsev;
 }
 
 // ================================================================ launchers
@@ -792,9 +829,9 @@ void launch_gather(const int* src, int64_t rows, int D, const void* a, void* a_o
 void launch_merge(const IndexCtx& C, int D, const int* heads_list, int n_heads, int n_rows, void* o, float* lse,
                   cudaStream_t st) {
   if (n_rows <= 0 || n_heads <= 0) return;
-  const int threads = n_rows * 32;
-  merge_kernel<<<dim3((threads + 255) / 256, n_heads), 256, 0, st>>>(C, D, heads_list, n_rows, (__nv_bfloat16*)o,
-                                                                     lse);
+  const long long threads = (long long)((n_rows + MERGE_R - 1) / MERGE_R) * 32;
+  merge_kernel<<<dim3((unsigned)((threads + 255) / 256), n_heads), 256, 0, st>>>(C, D, heads_list, n_rows,
+                                                                                 (__nv_bfloat16*)o, lse);
 }
 
 }  // namespace mmi

@@ -68,10 +68,13 @@ def lib():
         L.mmi_dense_prefill.argtypes = [P, vp, vp, vp, vp, vp, vp]
         L.mmi_export_index.argtypes = [P, C, vp, sz, i32, vp, ctypes.POINTER(sz), vp]
         L.mmi_sparse_fingerprint.argtypes = [P, C, vp, sz, vp, vp, vp, vp, vp]
+        L.mmi_plan_stats.argtypes = [P, C, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+        L.mmi_traffic_stats.argtypes = [P, C, vp, sz, ctypes.POINTER(ctypes.c_int64), vp]
         L.mmi_last_error.restype = ctypes.c_char_p
         L.mmi_version.restype = ctypes.c_char_p
         for fn in ("mmi_estimate_index", "mmi_permute", "mmi_sparse_prefill", "mmi_unpermute",
-                   "mmi_dense_prefill", "mmi_export_index", "mmi_sparse_fingerprint"):
+                   "mmi_dense_prefill", "mmi_export_index", "mmi_sparse_fingerprint", "mmi_plan_stats",
+                   "mmi_traffic_stats"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -127,6 +130,21 @@ def _need_cuda(*ts):
 # ------------------------------------------------------------------ C ABI mirrors
 def mmi_workspace_bytes(pb: Problem, cfgs: Sequence[HeadConfig]) -> int:
     return int(lib().mmi_workspace_bytes(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs)))
+
+
+def mmi_plan_stats(pb: Problem, cfgs: Sequence[HeadConfig]) -> dict:
+    """Host-only plan sizes (for algorithmic-traffic reporting)."""
+    out = (ctypes.c_int64 * 5)()
+    _check(lib().mmi_plan_stats(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), out, 5))
+    return dict(qg_rows=out[0], kg_rows=out[1], merge_heads=out[2], slabs=out[3], part_rows=out[4])
+
+
+def mmi_traffic_stats(pb: Problem, cfgs: Sequence[HeadConfig], ws, stream=None) -> dict:
+    """Rows moved by the permute step (reporting only; synchronises)."""
+    out = (ctypes.c_int64 * 4)()
+    _check(lib().mmi_traffic_stats(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws), ws.numel() * ws.element_size(), out,
+                                   _stream(stream)))
+    return dict(qg_read=out[0], qg_written=out[1], kg_read=out[2], kg_written=out[3])
 
 
 def mmi_estimate_index(pb, cfgs, q, k, modality, ws, stream=None):
