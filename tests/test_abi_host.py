@@ -94,3 +94,36 @@ def test_binding_refuses_cpu_fallback():
     except (RuntimeError, ValueError) as e:
         sp_err = e
     assert sp_err is not None
+
+
+@pytest.mark.parametrize("idx", [1, 3])
+def test_plan_stats_consistent_with_config(idx):
+    """mmi_plan_stats (host-only): one estimation slab per estimated pattern instance
+    (Grid / VS; per query modality for Q-/2D-boundary heads), merge heads = heads with
+    a multi-pass Grid (slash) instance, gathered rows padded to whole 128-row tiles."""
+    from paper_2504_16083_b200 import mmi_plan_stats
+    from synth.config import KIND_GRID, KIND_VSLASH
+    wl = build_workload(idx)
+    st = mmi_plan_stats(wl.problem, wl.heads)
+    assert st["qg_rows"] % 128 == 0 and st["kg_rows"] % 128 == 0
+    assert st["qg_rows"] > 0 and st["kg_rows"] > 0
+    n_est = sum(1 for h in wl.heads if any(p.kind in (KIND_GRID, KIND_VSLASH) for p in
+                                           ([h.intra[0]] if h.boundary in (0, 1) else
+                                            h.intra[:wl.problem.n_modalities] if h.boundary == 2 else
+                                            [q for row in h.pair for q in row])))
+    assert 1 <= st["slabs"]
+    assert st["slabs"] >= n_est
+    assert 0 <= st["merge_heads"] <= wl.problem.n_heads
+    if idx == 1:   # LongVILA-shaped: grid heads with slash lines need the LSE merge
+        n_slash = sum(1 for h in wl.heads if h.intra[0].kind == KIND_GRID and h.intra[0].use_slash)
+        assert st["merge_heads"] == n_slash
+
+
+def test_plan_stats_rejects_invalid():
+    from paper_2504_16083_b200.mmi import lib, to_c_problem, to_c_configs
+    pb = Problem(3, 2, 4096, 128)    # H % Hkv != 0
+    out = (ctypes.c_int64 * 5)()
+    st = lib().mmi_plan_stats(ctypes.byref(to_c_problem(pb)), to_c_configs([HeadConfig.no_boundary(full())] * 3),
+                              out, 5)
+    assert st != 0
+    assert lib().mmi_plan_stats(None, None, out, 5) != 0

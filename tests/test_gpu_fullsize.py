@@ -44,3 +44,22 @@ def test_fullsize_config(cfg):
     near = sum(r["index"]["near"] for r in report)
     print(f"config {cfg}: {len(report)} heads checked, near-ties {near}, "
           f"max err {max(r['max_err'] for r in report):.4f}")
+
+
+@pytest.mark.slow
+def test_fullsize_1m_sampled():
+    """BASELINE configs[4] (LongVILA-shaped, 1M tokens) in the bench's launch
+    configuration: one head of each pattern type (fixed-stride grid, searched grid,
+    grid with slash lines, A-shape), exact index + fingerprints + tolerance on sampled rows."""
+    wl = build_workload(4)
+    d = gen_qkv(wl, seed=4)
+    g = run_gpu(wl, d)
+    for h in (0, 1, 2, 3):
+        rows = _sample(wl, d, g, h, n_random=64)
+        if rows.size > 192:
+            rng = np.random.default_rng(h)
+            rows = np.unique(np.concatenate([rows[:32], rows[-32:], rng.choice(rows[32:-32], 128, replace=False)]))
+        res = check_head(wl, d, g, h, rows=rows)
+        assert not res["index"]["mismatch"], res
+        assert res["fp_count_ok"] and res["fp_sum_ok"] and res["fp_sum2_ok"], res
+        assert res["max_err"] <= TOL_MAX and res["mean_err"] <= TOL_MEAN, res
