@@ -148,6 +148,33 @@ def oracle_sample(wl, d, seed=0, n_rows=256, heads=None):
     return ms_layer, wall, cores, sample
 
 
+def _sdpa_sanity(q, k, v, G, stream):
+    """SURVEY 8(d.3) sanity: the same dense causal layer through torch SDPA's cuDNN and flash
+    backends (library kernels, timed beside the same-build comparator so it is not a strawman)."""
+    from torch.nn.attention import sdpa_kernel, SDPBackend
+    import torch.nn.functional as F
+    out = {}
+    qq = q.unsqueeze(0)
+    kk = k.repeat_interleave(G, dim=0).unsqueeze(0)
+    vv = v.repeat_interleave(G, dim=0).unsqueeze(0)
+    for name, be in (("cudnn", SDPBackend.CUDNN_ATTENTION), ("flash", SDPBackend.FLASH_ATTENTION)):
+        try:
+            with sdpa_kernel([be]):
+                F.scaled_dot_product_attention(qq, kk, vv, is_causal=True)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                F.scaled_dot_product_attention(qq, kk, vv, is_causal=True)
+                b.record(stream)
+                torch.cuda.synchronize()
+                out[name] = a.elapsed_time(b)
+        except Exception as ex:  # library backend unavailable for this shape / arch
+            out[name] = None
+            out[name + "_error"] = str(ex).splitlines()[0][:120] if str(ex) else type(ex).__name__
+    del kk, vv
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -301,7 +328,8 @@ def main():
         hbm["stages"][name] = {"bytes": int(nbytes), "GBps": gbs, "frac": (gbs / hbm_peak) if gbs else None, "bytes_def": how}
 
     # same-build dense comparator (a separate measurement, not in the timed steps)
-    dense_ms = None
+    dense_ms, dense_sota = None, None
+    G = pb.n_heads // pb.n_kv_heads
     want_dense = args.dense if args.dense >= 0 else int(pb.seq_len <= 262144)
     if want_dense:
         od = torch.empty_like(o)
@@ -315,6 +343,7 @@ def main():
         torch.cuda.synchronize()
         dense_ms = a.elapsed_time(b) / 2
         del od
+        dense_sota = _sdpa_sanity(q, k, v, G, stream) if rank == 0 else None
 
     # end to end through the public API with host buffers (pinned), per step
     e2e = None
@@ -366,6 +395,7 @@ def main():
             "stage_ms": stage,
             "dense_ms": dense_ms,
             "speedup_vs_dense": (dense_ms / ms) if dense_ms else None,
+            "dense_library_ms": dense_sota,
             "tile_density": tiles / dense_tiles,
             "roofline": roof, "hbm": hbm,
             "cpu_baseline": cpu,
