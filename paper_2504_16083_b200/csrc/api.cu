@@ -116,7 +116,7 @@ static IndexCtx make_ctx(const Plan& P, void* ws) {
   C.sort_keys = at<int>(ws, P.item_keys);
   C.sort_vals = at<int>(ws, P.item_vals);
   C.sort_vals_out = at<int>(ws, P.item_vals) + P.n_slots;
-  C.part_o = at<float>(ws, P.part_o);
+  C.part_o = at<__half>(ws, P.part_o);
   C.part_lse = at<float>(ws, P.part_lse);
   return C;
 }
@@ -246,7 +246,7 @@ static mmi_status run_sparse(const Plan& P, const mmi_problem* pb, void* ws, con
   A.labels = at<uint8_t>(ws, P.labels);
   A.o = o;
   A.lse = lse;
-  A.part_o = at<float>(ws, P.part_o);
+  A.part_o = at<__half>(ws, P.part_o);
   A.part_lse = at<float>(ws, P.part_lse);
   A.S = P.S;
   A.H = P.H;

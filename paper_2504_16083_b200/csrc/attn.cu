@@ -65,7 +65,10 @@ constexpr int CTRL_REGS = MMI_CTRL_REGS;  // setmaxnreg budgets: .inc only draws
 constexpr int SOFT_REGS = MMI_SOFT_REGS;  // inside the CTA's launch allocation, else it blocks forever
 static_assert(32 * NWARP_CTRL * CTRL_REGS + 32 * NWARP_SOFT * SOFT_REGS <= NTHREADS * LAUNCH_REGS,
               "setmaxnreg budget exceeds launch allocation");
-constexpr int NKP = 4;  // key-coordinate ring (positions / ranks of gathered key tiles that need them)
+constexpr int NKP = 4;
+// epilogue staging row: 64 B of output (32 16-bit columns) + 16 B pad, so that 8 consecutive rows
+// written by 8 lanes (one 16 B vector each) fall in distinct bank groups
+constexpr int EPI_STRIDE = 80;  // key-coordinate ring (positions / ranks of gathered key tiles that need them)
 
 // MMI_PROF builds (scratch/variants.sh only) accumulate per-phase SM clocks into g_prof
 #ifdef MMI_PROF
@@ -93,7 +96,8 @@ struct Smem {
   static constexpr int OFF_KRANK = OFF_KPOS + NKP * BLK * 4;
   static constexpr int OFF_SCHED = OFF_KRANK + NKP * BLK * 4;  // [SCHED_RING] x {idx, pad, WorkItem}: 128 B
   static constexpr int OFF_RI = OFF_SCHED + SCHED_RING * SCHED_ENTRY;     // [2] x {pos[256], rank[256]} of the item's rows
-  static constexpr int OFF_BAR = OFF_RI + 2 * 2 * 2 * BLK * 4;
+  static constexpr int OFF_EPI = OFF_RI + 2 * 2 * 2 * BLK * 4;  // [softmax warp] epilogue staging: 32 rows x EPI_STRIDE
+  static constexpr int OFF_BAR = OFF_EPI + NWARP_SOFT * 32 * EPI_STRIDE;
   // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2][2] p_full[2][2] o_full[2]
   // o_empty[2] pv_done[2] sched_full[R] sched_empty[R] kp_full[NKP] kp_empty[NKP]
   static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 14 + 2 * SCHED_RING + 2 * NKP + 4;
@@ -172,6 +176,23 @@ __device__ __forceinline__ int count_le(const int* a, int v) {
   for (int step = 64; step > 0; step >>= 1)
     if (a[i + step - 1] <= v) i += step;
   return i + ((i == BLK - 1 && a[BLK - 1] <= v) ? 1 : 0);
+}
+
+// three count_le searches in lockstep (independent shared-memory probes overlap their latency):
+// a1 = #{a <= v1}, b2 = #{b <= v2}, b3 = #{b <= v3}
+__device__ __forceinline__ void count_le3(const int* a, int v1, const int* b, int v2, int v3, int& a1, int& b2,
+                                          int& b3) {
+  int i = 0, j = 0, k = 0;
+#pragma unroll
+  for (int step = 64; step > 0; step >>= 1) {
+    const int x = a[i + step - 1], y = b[j + step - 1], z = b[k + step - 1];
+    if (x <= v1) i += step;
+    if (y <= v2) j += step;
+    if (z <= v3) k += step;
+  }
+  a1 = i + ((i == BLK - 1 && a[BLK - 1] <= v1) ? 1 : 0);
+  b2 = j + ((j == BLK - 1 && b[BLK - 1] <= v2) ? 1 : 0);
+  b3 = k + ((k == BLK - 1 && b[BLK - 1] <= v3) ? 1 : 0);
 }
 
 // 128 bits of a bitmap starting at bit `lo` (bits below 0 read as 0): out[w] bit i = bit(lo + 32w + i)
@@ -560,7 +581,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t n_sub = 0;  // sub-tiles this half has processed (= P V commits on pv_done[hf])
     const int G = P.H / P.Hkv;
     PROF_DECL(stot); PROF_DECL(sws); PROF_DECL(sld); PROF_DECL(smask); PROF_DECL(ssm); PROF_DECL(sresc);
-    PROF_DECL(spst); PROF_DECL(sepi); PROF_DECL(snt); PROF_DECL(snr); PROF_DECL(sfetch); PROF_DECL(sitem);
+    PROF_DECL(spst); PROF_DECL(sepi); PROF_DECL(snt); PROF_DECL(snr); PROF_DECL(sfetch); PROF_DECL(sitem); PROF_DECL(smword); PROF_DECL(sepw); PROF_DECL(sepl);
     [[maybe_unused]] const long long sprof_start = PROF_T();
     for (int i = 0;; ++i) {
       long long t0 = PROF_T();
@@ -624,12 +645,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int kv = it.head / G;
       SegIter si;
       si.init(P, it);
+      int c_inst = -1, c_sink = 0, c_local = 0;  // cached pattern parameters of the current instance
+      const uint32_t* c_sl = nullptr;
+      const uint32_t* c_vm = nullptr;
       PROF_ADD(sitem, t0);
       for (int t = 0; t < it.n_tiles; ++t) {
         const TileInfo e = si.next(P, it);
         const uint32_t space = e.space, pred = e.pred, role = e.role, rmode = e.rmode, inst = e.inst;
         const bool masked = pred || P.fingerprint;
         uint32_t mw[4] = {0u, 0u, 0u, 0u};  // admitted-key mask of the tile (bit c <-> key c)
+        t0 = PROF_T();
         if (masked) {
           const bool need_kp = space;
           if (need_kp) mbar_wait(kp_full + kps, kp_phase);
@@ -639,16 +664,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (!pred) {
               range_mask(mw, 0, BLK - 1);
             } else {
-              int sink = 0, local = 0;
-              const uint32_t* sl_bits = nullptr;
-              const uint32_t* vm_bits = nullptr;
-              if (!P.dense && role != R_TRUE) {
+              if (!P.dense && role != R_TRUE && (int)inst != c_inst) {
+                // pattern parameters of the tile's instance: reloaded only when the instance changes
                 const InstParam ip = P.insts[it.inst_base + inst];
-                sink = ip.sink;
-                local = ip.local;
-                if (ip.slash_word >= 0) sl_bits = P.bits + ip.slash_word;
-                if (ip.vmask_word >= 0) vm_bits = P.bits + ip.vmask_word;
+                c_inst = (int)inst;
+                c_sink = ip.sink;
+                c_local = ip.local;
+                c_sl = ip.slash_word >= 0 ? P.bits + ip.slash_word : nullptr;
+                c_vm = ip.vmask_word >= 0 ? P.bits + ip.vmask_word : nullptr;
               }
+              const int sink = c_sink, local = c_local;
+              const uint32_t* sl_bits = c_sl;
+              const uint32_t* vm_bits = c_vm;
               const int x = rmode ? xrank : xpos;
               // Keys of every view are ascending inside a tile, so each role is at most two
               // index ranges: [0, n_causal) intersected with the pattern's coordinate ranges.
@@ -660,9 +687,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 ybase = kbase;
               } else {
                 const int* yc = rmode ? (krank_s + kps * BLK) : kp;
-                n_causal = count_le(kp, xpos);
-                n_sink = (role == R_A || role == R_NOTA) ? count_le(yc, sink - 1) : 0;
-                n_lt_local = (role == R_A || role == R_NOTA) ? count_le(yc, x - local) : 0;
+                if (role == R_A || role == R_NOTA) {
+                  count_le3(kp, xpos, yc, sink - 1, x - local, n_causal, n_sink, n_lt_local);
+                } else {
+                  n_causal = count_le(kp, xpos);
+                  n_sink = n_lt_local = 0;
+                }
                 ybase = yc[0];
               }
               if (role == R_TRUE) {
@@ -707,6 +737,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
           }
         }
+        PROF_ADD(smword, t0);
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           t0 = PROF_T();
@@ -815,6 +846,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       t0 = PROF_T();
       // ---- epilogue ----
       mbar_wait(o_full + hf, o_phase);
+      PROF_ADD(sepw, t0);
       o_phase ^= 1;
       tc_fence_after();
       // no admitted key in this item <=> the running max never left -inf (the polynomial exp2
@@ -833,48 +865,61 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         continue;
       }
-      if (it.out_mode == OUT_FINAL) {
-        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(P.o) + ((size_t)it.head * P.S + xpos) * D;
+      // O (fp32, TMEM) -> 16-bit registers: bf16 for final rows, fp16 for partial rows (merged in fp32
+      // by merge_kernel).  O is released as soon as it is in registers.
+      const bool fin = (it.out_mode == OUT_FINAL);
+      uint32_t ov[D / 2];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tO + c * 32, r);
-          tmem_wait_ld();
-          if (c == D / 32 - 1) {
-            tc_fence_before();
-            mbar_arrive(o_empty + hf);  // O in registers: the next item's first P V may start
-          }
-          if (write) {
-            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tO + c * 32, r);
+        tmem_wait_ld();
+        if (fin) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint4 w;
-              w.x = pack_bf16(__uint_as_float(r[8 * j + 0]) * inv_l, __uint_as_float(r[8 * j + 1]) * inv_l);
-              w.y = pack_bf16(__uint_as_float(r[8 * j + 2]) * inv_l, __uint_as_float(r[8 * j + 3]) * inv_l);
-              w.z = pack_bf16(__uint_as_float(r[8 * j + 4]) * inv_l, __uint_as_float(r[8 * j + 5]) * inv_l);
-              w.w = pack_bf16(__uint_as_float(r[8 * j + 6]) * inv_l, __uint_as_float(r[8 * j + 7]) * inv_l);
-              dst[j] = w;
-            }
-          }
+          for (int j = 0; j < 16; ++j)
+            ov[c * 16 + j] = pack_bf16(__uint_as_float(r[2 * j]) * inv_l, __uint_as_float(r[2 * j + 1]) * inv_l);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            ov[c * 16 + j] = pack_f16(__uint_as_float(r[2 * j]) * inv_l, __uint_as_float(r[2 * j + 1]) * inv_l);
         }
+      }
+      tc_fence_before();
+      mbar_arrive(o_empty + hf);  // the next item's first P V of this half may start
+      PROF_ADD(sepl, t0);
+      // destination row (0: not written).  Partial rows are always written (zeros for invalid rows:
+      // the merge weights them by exp(-inf) = 0, which must not meet a NaN).
+      unsigned long long dst = 0;
+      if (fin) {
+        if (write) dst = reinterpret_cast<unsigned long long>(reinterpret_cast<__nv_bfloat16*>(P.o) +
+                                                              ((size_t)it.head * P.S + xpos) * D);
+      } else {
+        dst = reinterpret_cast<unsigned long long>(P.part_o + (size_t)(it.out_row0 + hf * BLK + row) * D);
+      }
+      // Thread-per-row stores would touch 32 rows (32 L1 wavefronts) per instruction; instead each
+      // 64-byte column chunk of the warp's 32 rows is transposed through shared memory so that one
+      // 16-byte store instruction writes 8 rows x 64 contiguous bytes.
+      unsigned long long dsts[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dsts[k] = __shfl_sync(0xffffffffu, dst, k * 8 + (lane >> 2));
+      const uint32_t ebuf = smem_u32(smem + L::OFF_EPI + (warp - NWARP_CTRL) * 32 * EPI_STRIDE);
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          st_shared_v4(ebuf + lane * EPI_STRIDE + q * 16, ov[c * 16 + 4 * q], ov[c * 16 + 4 * q + 1],
+                       ov[c * 16 + 4 * q + 2], ov[c * 16 + 4 * q + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint4 w = ld_shared_v4(ebuf + (k * 8 + (lane >> 2)) * EPI_STRIDE + (lane & 3) * 16);
+          if (dsts[k]) *reinterpret_cast<uint4*>(dsts[k] + c * 64 + (lane & 3) * 16) = w;
+        }
+        __syncwarp();
+      }
+      if (fin) {
         if (write && P.lse) P.lse[(size_t)it.head * P.S + xpos] = lse_v;
       } else {
-        float* prow = P.part_o + (size_t)(it.out_row0 + hf * BLK + row) * D;
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tO + c * 32, r);
-          tmem_wait_ld();
-          if (c == D / 32 - 1) {
-            tc_fence_before();
-            mbar_arrive(o_empty + hf);
-          }
-          float4* dst = reinterpret_cast<float4*>(prow + c * 32);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(__uint_as_float(r[4 * j]) * inv_l, __uint_as_float(r[4 * j + 1]) * inv_l,
-                                 __uint_as_float(r[4 * j + 2]) * inv_l, __uint_as_float(r[4 * j + 3]) * inv_l);
-        }
         P.part_lse[it.out_row0 + hf * BLK + row] = valid ? lse_v : -INFINITY;
       }
       if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 6] = gtimer();
@@ -884,7 +929,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       PROF_FLUSH(8, stot); PROF_FLUSH(9, sws); PROF_FLUSH(10, sld); PROF_FLUSH(11, smask); PROF_FLUSH(12, ssm);
       PROF_FLUSH(13, sresc); PROF_FLUSH(14, spst); PROF_FLUSH(15, sepi); PROF_FLUSH(16, snt); PROF_FLUSH(17, snr);
-      PROF_FLUSH(18, sfetch); PROF_FLUSH(19, sitem);
+      PROF_FLUSH(18, sfetch); PROF_FLUSH(19, sitem); PROF_FLUSH(20, smword); PROF_FLUSH(21, sepw); PROF_FLUSH(22, sepl);
     }
   }
   tc_fence_before();

@@ -774,8 +774,8 @@ __global__ void merge_kernel(IndexCtx C, int D, const int* __restrict__ heads_li
       a[r][c] = make_float2(0.f, 0.f);
       b[r][c] = make_float2(0.f, 0.f);
       if (c < nc && p >= 0) {
-        a[r][c] = *reinterpret_cast<const float2*>(C.part_o + q0 * D + c * 64 + 2 * lane);
-        if (q1 >= 0) b[r][c] = *reinterpret_cast<const float2*>(C.part_o + q1 * D + c * 64 + 2 * lane);
+        a[r][c] = __half22float2(*reinterpret_cast<const __half2*>(C.part_o + q0 * D + c * 64 + 2 * lane));
+        if (q1 >= 0) b[r][c] = __half22float2(*reinterpret_cast<const __half2*>(C.part_o + q1 * D + c * 64 + 2 * lane));
       }
     }
   }

@@ -35,7 +35,7 @@ struct IndexCtx {
   int* sort_keys;
   int* sort_vals;
   const int* sort_vals_out;
-  const float* part_o;
+  const __half* part_o;
   const float* part_lse;
 };
 

@@ -2,6 +2,7 @@
 // kernels and the block-sparse attention kernel.  Not part of the public ABI.
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace mmi {
@@ -70,7 +71,7 @@ struct AttnParams {
   const uint8_t* labels;    // modality label by original position [S]
   void* o;                  // bf16 [H, S, D]
   float* lse;               // [H, S] (nullable)
-  float* part_o;            // fp32 partial rows [rows, D]
+  __half* part_o;           // fp16 partial rows [rows, D] (normalised O of one pass; merged in fp32)
   float* part_lse;
   int32_t S, H, Hkv, D;
   float scale_log2;         // tau * log2(e)

@@ -417,7 +417,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
   reg(P.inst_params, sizeof(InstParam) * P.insts.size());
   reg(P.sort_tmp, P.sort_tmp_bytes);
   reg(P.scan_tmp, P.scan_tmp_bytes);
-  reg(P.part_o, sizeof(float) * (size_t)std::max<int64_t>(P.part_rows, 1) * P.D);
+  reg(P.part_o, sizeof(uint16_t) * (size_t)std::max<int64_t>(P.part_rows, 1) * P.D);  // fp16
   reg(P.part_lse, sizeof(float) * (size_t)std::max<int64_t>(P.part_rows, 1));
   P.total = off;
   return MMI_OK;

@@ -31,14 +31,17 @@ for _ in range(5):
     e0.record(); sp.sparse(q, k, v, o); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 tiles = sp.total_tiles()
+import struct
+from paper_2504_16083_b200.mmi import mmi_export_index
+n_items = sum(mmi_export_index(pb, sp.cfgs, sp.ws, h).tolist()[-4] for h in range(pb.n_heads))
 ms = float(np.median(ts))
-out = {"lib": os.environ.get("MMI_LIB", "libmmi.so"), "workload": w, "sparse_ms": ms, "tiles": tiles,
+out = {"lib": os.environ.get("MMI_LIB", "libmmi.so"), "workload": w, "sparse_ms": ms, "tiles": tiles, "items": n_items,
        "tflops": tiles * 4 * 128 * 128 * pb.head_dim / ms / 1e9}
 if prof:
     prof(buf, 1)
     names = ["mma_tot", "mma_wait_p", "mma_wait_k", "mma_wait_v", "mma_wait_q", "mma_wait_o", "mma_nt", "",
              "sm_tot", "sm_wait_s", "sm_ld", "sm_mask", "sm_softmax", "sm_rescale", "sm_pstore", "sm_epi",
-             "sm_nsub", "sm_nresc", "sm_fetch", "sm_item"]
+             "sm_nsub", "sm_nresc", "sm_fetch", "sm_item", "sm_mword", "sm_epi_wait", "sm_epi_ld"]
     tot = {n: buf[i] for i, n in enumerate(names) if n}
     out["prof_frac"] = {n: round(tot[n] / max(tot["mma_tot" if n.startswith("mma") else "sm_tot"], 1), 4)
                         for n in tot if not n.endswith("tot") and n not in ("mma_nt", "sm_nsub", "sm_nresc")}
