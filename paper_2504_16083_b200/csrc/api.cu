@@ -268,6 +268,8 @@ static mmi_status run_sparse(const Plan& P, const mmi_problem* pb, void* ws, con
   L.qg_rows = P.qg_rows;
   L.kv_rows = (long long)P.Hkv * P.S;
   L.kvg_rows = P.kg_rows;
+  L.o_rows = (long long)P.H * P.S;
+  L.part_rows = P.part_rows;
   int te = 0;
   cudaError_t e = launch_attn(L, A, P.n_slots, s, &te);
   if (te) return fail(MMI_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", te);
@@ -336,6 +338,7 @@ extern "C" mmi_status mmi_dense_prefill(const mmi_problem* pb, const void* q, co
   L.v = v;
   L.q_rows = (long long)pb->n_heads * pb->seq_len;
   L.kv_rows = (long long)pb->n_kv_heads * pb->seq_len;
+  L.o_rows = (long long)pb->n_heads * pb->seq_len;
   int te = 0;
   const int nb = (pb->seq_len + 127) / 128;
   cudaError_t e = launch_attn(L, A, pb->n_heads * nb, (cudaStream_t)stream, &te);

@@ -68,7 +68,8 @@ static_assert(32 * NWARP_CTRL * CTRL_REGS + 32 * NWARP_SOFT * SOFT_REGS <= NTHRE
 constexpr int NKP = 4;
 // epilogue staging row: 64 B of output (32 16-bit columns) + 16 B pad, so that 8 consecutive rows
 // written by 8 lanes (one 16 B vector each) fall in distinct bank groups
-constexpr int EPI_STRIDE = 80;  // key-coordinate ring (positions / ranks of gathered key tiles that need them)
+constexpr int EPI_STRIDE = 80;
+static_assert((32 * EPI_STRIDE) % 512 == 0, "staging buffers must stay 512 B aligned");  // key-coordinate ring (positions / ranks of gathered key tiles that need them)
 
 // MMI_PROF builds (scratch/variants.sh only) accumulate per-phase SM clocks into g_prof
 #ifdef MMI_PROF
@@ -96,7 +97,8 @@ struct Smem {
   static constexpr int OFF_KRANK = OFF_KPOS + NKP * BLK * 4;
   static constexpr int OFF_SCHED = OFF_KRANK + NKP * BLK * 4;  // [SCHED_RING] x {idx, pad, WorkItem}: 128 B
   static constexpr int OFF_RI = OFF_SCHED + SCHED_RING * SCHED_ENTRY;     // [2] x {pos[256], rank[256]} of the item's rows
-  static constexpr int OFF_EPI = OFF_RI + 2 * 2 * 2 * BLK * 4;  // [softmax warp] epilogue staging: 32 rows x EPI_STRIDE
+  // [softmax warp] epilogue staging, 32 rows x EPI_STRIDE each, 512 B aligned (TMA 64B-swizzle atom)
+  static constexpr int OFF_EPI = (OFF_RI + 2 * 2 * 2 * BLK * 4 + 1023) & ~1023;
   static constexpr int OFF_BAR = OFF_EPI + NWARP_SOFT * 32 * EPI_STRIDE;
   // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2][2] p_full[2][2] o_full[2]
   // o_empty[2] pv_done[2] sched_full[R] sched_empty[R] kp_full[NKP] kp_empty[NKP]
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     attn_kernel(const __grid_constant__ CUtensorMap tmQo, const __grid_constant__ CUtensorMap tmQg,
                 const __grid_constant__ CUtensorMap tmKo, const __grid_constant__ CUtensorMap tmKg,
                 const __grid_constant__ CUtensorMap tmVo, const __grid_constant__ CUtensorMap tmVg,
+                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmPart,
                 const AttnParams P) {
   using L = Smem<D>;
   constexpr int KST = L::KST, VST = L::VST;
@@ -896,26 +899,55 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       } else {
         dst = reinterpret_cast<unsigned long long>(P.part_o + (size_t)(it.out_row0 + hf * BLK + row) * D);
       }
-      // Thread-per-row stores would touch 32 rows (32 L1 wavefronts) per instruction; instead each
-      // 64-byte column chunk of the warp's 32 rows is transposed through shared memory so that one
-      // 16-byte store instruction writes 8 rows x 64 contiguous bytes.
-      unsigned long long dsts[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) dsts[k] = __shfl_sync(0xffffffffu, dst, k * 8 + (lane >> 2));
       const uint32_t ebuf = smem_u32(smem + L::OFF_EPI + (warp - NWARP_CTRL) * 32 * EPI_STRIDE);
+      const int wrow0 = (warp % 4) * 32;  // first row of this warp in the half (its TMEM lane base)
+      if (!fin || (!it.q_gathered && __all_sync(0xffffffffu, write))) {
+        // The warp's 32 rows are contiguous in the destination (partial rows, or final rows of an
+        // original-order block that are all written): each 32-column chunk is staged in the TMA
+        // 64B-swizzle layout (16 B chunk q of row r at q ^ ((r >> 1) & 3): conflict-free) and written
+        // by one TMA tensor store, asynchronously.
+        const CUtensorMap* tm = fin ? &tmO : &tmPart;
+        const int grow = (fin ? it.q_row0 : it.out_row0) + hf * BLK + wrow0;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < D / 32; ++c) {
+          if (c > 0) {
+            if (lane == 0) bulk_wait_read0();  // the previous chunk has left the buffer
+            __syncwarp();
+          }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          st_shared_v4(ebuf + lane * EPI_STRIDE + q * 16, ov[c * 16 + 4 * q], ov[c * 16 + 4 * q + 1],
-                       ov[c * 16 + 4 * q + 2], ov[c * 16 + 4 * q + 3]);
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint4 w = ld_shared_v4(ebuf + (k * 8 + (lane >> 2)) * EPI_STRIDE + (lane & 3) * 16);
-          if (dsts[k]) *reinterpret_cast<uint4*>(dsts[k] + c * 64 + (lane & 3) * 16) = w;
+          for (int q = 0; q < 4; ++q)
+            st_shared_v4(ebuf + lane * 64 + ((q ^ ((lane >> 1) & 3)) * 16), ov[c * 16 + 4 * q],
+                         ov[c * 16 + 4 * q + 1], ov[c * 16 + 4 * q + 2], ov[c * 16 + 4 * q + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(tm, ebuf, c * 32, grow);
+            bulk_commit();
+          }
         }
+        if (lane == 0) bulk_wait_read0();  // staging buffer free for the next item
         __syncwarp();
+      } else {
+        // scattered rows: thread-per-row stores would touch 32 rows (32 L1 wavefronts) per
+        // instruction; instead each 64-byte column chunk of the warp's 32 rows is transposed through
+        // shared memory so that one 16-byte store instruction writes 8 rows x 64 contiguous bytes.
+        unsigned long long dsts[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dsts[k] = __shfl_sync(0xffffffffu, dst, k * 8 + (lane >> 2));
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            st_shared_v4(ebuf + lane * EPI_STRIDE + q * 16, ov[c * 16 + 4 * q], ov[c * 16 + 4 * q + 1],
+                         ov[c * 16 + 4 * q + 2], ov[c * 16 + 4 * q + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint4 w = ld_shared_v4(ebuf + (k * 8 + (lane >> 2)) * EPI_STRIDE + (lane & 3) * 16);
+            if (dsts[k]) *reinterpret_cast<uint4*>(dsts[k] + c * 64 + (lane & 3) * 16) = w;
+          }
+          __syncwarp();
+        }
       }
       if (fin) {
         if (write && P.lse) P.lse[(size_t)it.head * P.S + xpos] = lse_v;
@@ -925,6 +957,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 6] = gtimer();
       PROF_ADD(sepi, t0);
     }
+    if (lane == 0) bulk_wait0();  // this warp's TMA output stores are complete
     PROF_ADD(stot, sprof_start);
     if (lane == 0) {
       PROF_FLUSH(8, stot); PROF_FLUSH(9, sws); PROF_FLUSH(10, sld); PROF_FLUSH(11, smask); PROF_FLUSH(12, ssm);
@@ -983,6 +1016,20 @@ int make_tmap_rows(CUtensorMap* m, const void* base, long long rows, int D) {
   return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
+// rows x D 16-bit row-major output; box = 32 rows x 32 columns (64 B), 64B swizzle (epilogue staging)
+static int make_tmap_out(CUtensorMap* m, const void* base, long long rows, int D, CUtensorMapDataType dt) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return -1;
+  if (rows <= 0) rows = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
 static int g_num_sms = 0;
 // work-item counters for launches without a workspace (dense comparator); rotating slots
 __device__ unsigned int g_sched_counters[64];
@@ -990,7 +1037,7 @@ static unsigned g_sched_slot = 0;
 
 cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hint, cudaStream_t stream,
                         int* tmap_err) {
-  CUtensorMap m[6];
+  CUtensorMap m[8];
   int e = 0;
   e |= make_tmap_rows(&m[0], L.q, L.q_rows, P.D);
   e |= make_tmap_rows(&m[1], L.qg ? L.qg : L.q, L.qg ? L.qg_rows : L.q_rows, P.D);
@@ -998,6 +1045,10 @@ cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hi
   e |= make_tmap_rows(&m[3], L.kg ? L.kg : L.k, L.kg ? L.kvg_rows : L.kv_rows, P.D);
   e |= make_tmap_rows(&m[4], L.v, L.kv_rows, P.D);
   e |= make_tmap_rows(&m[5], L.vg ? L.vg : L.v, L.vg ? L.kvg_rows : L.kv_rows, P.D);
+  // output maps (epilogue TMA stores): bf16 O [H*S, D] and fp16 partial rows [part_rows, D]
+  e |= make_tmap_out(&m[6], P.o ? P.o : L.q, P.o ? L.o_rows : L.q_rows, P.D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
+  e |= make_tmap_out(&m[7], L.part_rows > 0 ? (const void*)P.part_o : L.q, L.part_rows > 0 ? L.part_rows : L.q_rows,
+                     P.D, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
   if (tmap_err) *tmap_err = e;
   if (e) return cudaErrorInvalidValue;
   if (!g_num_sms) {
@@ -1018,11 +1069,11 @@ cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hi
   if (P.D == 128) {
     auto kfn = attn_kernel<128>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::ALLOC);
-    kfn<<<grid, NTHREADS, Smem<128>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], Pl);
+    kfn<<<grid, NTHREADS, Smem<128>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], Pl);
   } else {
     auto kfn = attn_kernel<64>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<64>::ALLOC);
-    kfn<<<grid, NTHREADS, Smem<64>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], Pl);
+    kfn<<<grid, NTHREADS, Smem<64>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], Pl);
   }
   return cudaGetLastError();
 }

@@ -85,6 +85,7 @@ struct AttnParams {
 struct AttnLaunch {
   const void *q, *qg, *k, *kg, *v, *vg;   // original and gathered Q/K/V spaces (bf16 rows of D)
   long long q_rows, qg_rows, kv_rows, kvg_rows;
+  long long o_rows = 0, part_rows = 0;   // rows of the bf16 output [H*S] and of the fp16 partial buffer
 };
 
 cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hint, cudaStream_t stream,
