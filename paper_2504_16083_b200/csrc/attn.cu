@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t v_base = smem_u32(smem + L::OFF_V);
         int ks = 0, vs = 0;
         uint32_t k_phase = 0, v_phase = 0, q_phase = 0;
-        uint32_t p_phase[4] = {0, 0, 0, 0}, o_phase[2] = {0, 0};
+        uint32_t p_bits = 0, o_bits = 0;  // phase bits: P per (half, slot), O per half (no indexed arrays: they would live in local memory)
         PROF_DECL(wp); PROF_DECL(wk); PROF_DECL(wv); PROF_DECL(wq); PROF_DECL(wo); PROF_DECL(tot); PROF_DECL(nt);
         [[maybe_unused]] const long long prof_start = PROF_T();
         for (int i = 0;; ++i) {
@@ -495,11 +495,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           auto issue_pv = [&](int hf, int j) {
             const int u = j & 1;
             long long t0 = PROF_T();
-            mbar_wait(p_full + 2 * hf + u, p_phase[2 * hf + u]);
+            mbar_wait(p_full + 2 * hf + u, (p_bits >> (2 * hf + u)) & 1u);
             PROF_ADD(wp, t0);
-            p_phase[2 * hf + u] ^= 1;
+            p_bits ^= 1u << (2 * hf + u);
             t0 = PROF_T();
-            if (j == 0) mbar_wait(o_empty + hf, o_phase[hf] ^ 1);  // previous item's epilogue read O_h
+            if (j == 0) mbar_wait(o_empty + hf, ((o_bits >> hf) & 1u) ^ 1u);  // previous item's epilogue read O_h
             PROF_ADD(wo, t0);
             tc_fence_after();
 #pragma unroll
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             umma_commit(pv_done + hf);  // lets the softmax rescale O_h once this P V has landed
             if (j == nsub - 1) {
               umma_commit(o_full + hf);
-              o_phase[hf] ^= 1;
+              o_bits ^= 1u << hf;
             }
           };
           // prologue: both sub-tiles of key tile 0 for every half

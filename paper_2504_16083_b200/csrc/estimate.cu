@@ -534,7 +534,9 @@ __device__ __forceinline__ void grid_window(const DInst& x, const int* sinfo, co
 // and the per-chunk sums are flushed with 64-bit integer atomics.  Integer
 // addition is associative, so the fold is exact and order-independent
 // (deterministic) for any schedule.
-constexpr int FOLD_CHUNK = 4096;
+// keys per CTA: one fixed-point atomic per (stride, phase) and chunk, so larger chunks mean fewer
+// L2 atomics (the fold's limiter at 4096); 96 KB of u64 keeps two CTAs per SM
+constexpr int FOLD_CHUNK = 12288;
 constexpr int FOLD_SG = 32;  // strides per CTA
 constexpr double FX52 = 4503599627370496.0;
 
@@ -544,7 +546,8 @@ __global__ void __launch_bounds__(256) grid_acc_kernel(const DInst* __restrict__
                                                        const float* __restrict__ c_rank, int S, int S_pad,
                                                        const int64_t* __restrict__ acc_off,
                                                        unsigned long long* __restrict__ acc) {
-  __shared__ unsigned long long chunk[FOLD_CHUNK];  // c over this part of W, 2^-52 fixed point
+  extern __shared__ unsigned long long fold_smem[];
+  unsigned long long* chunk = fold_smem;  // [FOLD_CHUNK] c over this part of W, 2^-52 fixed point
   __shared__ unsigned long long part[256];
   const int gi = blockIdx.z;
   const DInst x = insts[grid_inst[gi]];
@@ -700,7 +703,9 @@ void launch_grid(const DInst* insts, const int* grid_inst, int n_grid, int max_n
                                                                    c_rank, S_pad);
   const int n_sg = (max_ncand + FOLD_SG - 1) / FOLD_SG;
   const int n_ch = (S + FOLD_CHUNK - 1) / FOLD_CHUNK;
-  grid_acc_kernel<<<dim3(n_sg, n_ch, n_grid), 256, 0, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S,
+  const int fold_smem = FOLD_CHUNK * (int)sizeof(unsigned long long);
+  cudaFuncSetAttribute(grid_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fold_smem);
+  grid_acc_kernel<<<dim3(n_sg, n_ch, n_grid), 256, fold_smem, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S,
                                                               S_pad, acc_off, acc);
   grid_eval_kernel<<<dim3(max_ncand, n_grid), 256, 0, st>>>(insts, grid_inst, sinfo, info, S, acc_off, acc, part, res);
   grid_pick_kernel<<<n_grid, 1024, 0, st>>>(insts, grid_inst, part, res);

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "estimate.h"
 #include "index.h"
@@ -705,12 +706,16 @@ __global__ void gather_rows_kernel(const int* __restrict__ src, int64_t rows, co
 }
 
 // ================================================================ merge (a8)
-// One warp merges MERGE_R rows: lanes 0..R-1 resolve the rows' metadata (a chain of
-// dependent loads: modality position, instance, grid result, residue-class offset) in
-// parallel, then all partial-row loads of the R rows are issued before any use.
-constexpr int MERGE_R = 4;
-__global__ void merge_kernel(IndexCtx C, int D, const int* __restrict__ heads_list, int n_rows,
+// One warp merges MERGE_R = 32 rows: lane r resolves row r's metadata (a chain of dependent
+// loads: modality position, instance, grid result, residue-class offset), then the rows' data
+// move in batches of MERGE_B rows whose partial-row loads are all issued before any use; each
+// lane owns CPL contiguous columns (D = 32 CPL), so a row is one 32-lane vector access.
+constexpr int MERGE_R = 32;
+constexpr int MERGE_B = 8;
+template <int CPL>
+__global__ void merge_kernel(IndexCtx C, const int* __restrict__ heads_list, int n_rows,
                              __nv_bfloat16* __restrict__ o, float* __restrict__ lse) {
+  constexpr int D = 32 * CPL;
   const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   const int i_base = warp_g * MERGE_R;
@@ -762,35 +767,37 @@ __global__ void merge_kernel(IndexCtx C, int D, const int* __restrict__ heads_li
       pos = -1;
     }
   }
-  constexpr int NC = 2;  // 64-column chunks per row at D = 128 (1 used at D = 64); a float2 per lane each
-  float2 a[MERGE_R][NC], b[MERGE_R][NC];
-  const int nc = D / 64;
+  using VH = typename std::conditional<CPL == 4, uint2, uint32_t>::type;  // CPL fp16 / bf16 values
+#pragma unroll 1
+  for (int r0 = 0; r0 < MERGE_R; r0 += MERGE_B) {
+    VH a[MERGE_B], b[MERGE_B];
 #pragma unroll
-  for (int r = 0; r < MERGE_R; ++r) {
-    const int p = __shfl_sync(0xffffffffu, pos, r);
-    const long long q0 = __shfl_sync(0xffffffffu, j0, r), q1 = __shfl_sync(0xffffffffu, j1, r);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      a[r][c] = make_float2(0.f, 0.f);
-      b[r][c] = make_float2(0.f, 0.f);
-      if (c < nc && p >= 0) {
-        a[r][c] = __half22float2(*reinterpret_cast<const __half2*>(C.part_o + q0 * D + c * 64 + 2 * lane));
-        if (q1 >= 0) b[r][c] = __half22float2(*reinterpret_cast<const __half2*>(C.part_o + q1 * D + c * 64 + 2 * lane));
+    for (int r = 0; r < MERGE_B; ++r) {
+      const int p = __shfl_sync(0xffffffffu, pos, r0 + r);
+      const long long q0 = __shfl_sync(0xffffffffu, j0, r0 + r), q1 = __shfl_sync(0xffffffffu, j1, r0 + r);
+      a[r] = VH{};
+      b[r] = VH{};
+      if (p >= 0) {
+        a[r] = *reinterpret_cast<const VH*>(C.part_o + q0 * D + CPL * lane);
+        if (q1 >= 0) b[r] = *reinterpret_cast<const VH*>(C.part_o + q1 * D + CPL * lane);
       }
     }
-  }
 #pragma unroll
-  for (int r = 0; r < MERGE_R; ++r) {
-    const int p = __shfl_sync(0xffffffffu, pos, r);
-    if (p < 0) continue;
-    const float x0 = __shfl_sync(0xffffffffu, w0, r), x1 = __shfl_sync(0xffffffffu, w1, r);
-    const float xi = __shfl_sync(0xffffffffu, inv, r);
-    __nv_bfloat16* orow = o + ((size_t)h * C.S + p) * D;
+    for (int r = 0; r < MERGE_B; ++r) {
+      const int p = __shfl_sync(0xffffffffu, pos, r0 + r);
+      const float x0 = __shfl_sync(0xffffffffu, w0, r0 + r), x1 = __shfl_sync(0xffffffffu, w1, r0 + r);
+      const float xi = __shfl_sync(0xffffffffu, inv, r0 + r);
+      if (p < 0) continue;
+      const __half2* ha = reinterpret_cast<const __half2*>(&a[r]);
+      const __half2* hb = reinterpret_cast<const __half2*>(&b[r]);
+      VH out;
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&out);
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      if (c >= nc) break;
-      const float v0 = (a[r][c].x * x0 + b[r][c].x * x1) * xi, v1 = (a[r][c].y * x0 + b[r][c].y * x1) * xi;
-      *reinterpret_cast<__nv_bfloat162*>(orow + c * 64 + 2 * lane) = __floats2bfloat162_rn(v0, v1);
+      for (int c = 0; c < CPL / 2; ++c) {
+        const float2 fa = __half22float2(ha[c]), fb = __half22float2(hb[c]);
+        ob[c] = __floats2bfloat162_rn((fa.x * x0 + fb.x * x1) * xi, (fa.y * x0 + fb.y * x1) * xi);
+      }
+      *reinterpret_cast<VH*>(o + ((size_t)h * C.S + p) * D + CPL * lane) = out;
     }
   }
   if (lane < MERGE_R && pos >= 0 && lse) lse[(size_t)h * C.S + pos] = lsev;
@@ -830,8 +837,11 @@ void launch_merge(const IndexCtx& C, int D, const int* heads_list, int n_heads, 
                   cudaStream_t st) {
   if (n_rows <= 0 || n_heads <= 0) return;
   const long long threads = (long long)((n_rows + MERGE_R - 1) / MERGE_R) * 32;
-  merge_kernel<<<dim3((unsigned)((threads + 255) / 256), n_heads), 256, 0, st>>>(C, D, heads_list, n_rows,
-                                                                                 (__nv_bfloat16*)o, lse);
+  const dim3 grid((unsigned)((threads + 255) / 256), n_heads);
+  if (D == 128)
+    merge_kernel<4><<<grid, 256, 0, st>>>(C, heads_list, n_rows, (__nv_bfloat16*)o, lse);
+  else
+    merge_kernel<2><<<grid, 256, 0, st>>>(C, heads_list, n_rows, (__nv_bfloat16*)o, lse);
 }
 
 }  // namespace mmi
