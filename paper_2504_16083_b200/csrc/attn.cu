@@ -767,7 +767,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
           PROF_ADD(sld, t0);
           t0 = PROF_T();
+          // (sub-tiles every row of the warp fully admits skip the select: diagonal / sink / local
+          // tiles are mostly all-or-nothing per 64 keys)
+#ifdef MMI_NO_MASKSKIP
           if (masked) {
+#else
+          if (masked && !__all_sync(0xffffffffu, (mw[2 * u] & mw[2 * u + 1]) == 0xffffffffu)) {
+#endif
 #pragma unroll
             for (int c = 0; c < 64; ++c)
               if (!((mw[2 * u + (c >> 5)] >> (c & 31)) & 1u)) s[c] = -INFINITY;

@@ -534,9 +534,12 @@ __device__ __forceinline__ void grid_window(const DInst& x, const int* sinfo, co
 // and the per-chunk sums are flushed with 64-bit integer atomics.  Integer
 // addition is associative, so the fold is exact and order-independent
 // (deterministic) for any schedule.
-// keys per CTA: one fixed-point atomic per (stride, phase) and chunk, so larger chunks mean fewer
-// L2 atomics (the fold's limiter at 4096); 96 KB of u64 keeps two CTAs per SM
-constexpr int FOLD_CHUNK = 12288;
+// keys per CTA (u64 fixed point in shared memory): one atomic per (stride, phase) and chunk; the
+// fold is issue-bound, so occupancy matters more than the atomic count (12288 measured slower)
+#ifndef MMI_FOLD_CHUNK
+#define MMI_FOLD_CHUNK 4096
+#endif
+constexpr int FOLD_CHUNK = MMI_FOLD_CHUNK;
 constexpr int FOLD_SG = 32;  // strides per CTA
 constexpr double FX52 = 4503599627370496.0;
 

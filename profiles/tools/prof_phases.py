@@ -30,12 +30,18 @@ for _ in range(5):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); sp.sparse(q, k, v, o); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
+lab_ = lab
+te = []
+for _ in range(5):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); sp.estimate(q, k, lab_); e1.record(); torch.cuda.synchronize()
+    te.append(e0.elapsed_time(e1))
 tiles = sp.total_tiles()
 import struct
 from paper_2504_16083_b200.mmi import mmi_export_index
 n_items = sum(mmi_export_index(pb, sp.cfgs, sp.ws, h).tolist()[-4] for h in range(pb.n_heads))
 ms = float(np.median(ts))
-out = {"lib": os.environ.get("MMI_LIB", "libmmi.so"), "workload": w, "sparse_ms": ms, "tiles": tiles, "items": n_items,
+out = {"lib": os.environ.get("MMI_LIB", "libmmi.so"), "workload": w, "sparse_ms": ms, "estimate_ms": float(np.median(te)), "tiles": tiles, "items": n_items,
        "tflops": tiles * 4 * 128 * 128 * pb.head_dim / ms / 1e9}
 if prof:
     prof(buf, 1)
