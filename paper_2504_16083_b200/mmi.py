@@ -258,18 +258,34 @@ def dense_prefill(pb: Problem, q, k, v, o=None, lse=None, stream=None):
 
 
 class HostSparsePrefill:
-    """End-to-end public call with HOST tensors: pinned host -> device copies of
-    the step's inputs, the four C-ABI calls, and a device -> host copy of the
-    output, all on one stream."""
+    """End-to-end sparse pre-fill from pinned HOST buffers: each call copies the
+    step's inputs host -> device, runs the four C-ABI calls and copies O back.
 
-    def __init__(self, pb: Problem, cfgs: List[HeadConfig], device="cuda"):
-        self.sp = SparsePrefill(pb, cfgs, device)
+    Heads are independent (Alg.1-3 act per head), so the layer is processed in
+    chunks of whole KV-head groups, one stream each: the host -> device copy of
+    chunk c + 1 and the device -> host copy of chunk c - 1 run while chunk c
+    computes (the copy engines are full duplex).  Every chunk
+    is the same library call on a sub-problem, so O is identical to the
+    one-shot call.  The caller's stream waits for every chunk before returning."""
+
+    def __init__(self, pb: Problem, cfgs: List[HeadConfig], device="cuda", n_chunks: Optional[int] = None):
         H, Hkv, S, D = pb.n_heads, pb.n_kv_heads, pb.seq_len, pb.head_dim
+        G = H // Hkv
+        n = max(1, min(Hkv, n_chunks if n_chunks else 4))
+        self.pb, self.chunks = pb, []
+        for c in range(n):
+            g0, g1 = c * Hkv // n, (c + 1) * Hkv // n
+            if g1 <= g0:
+                continue
+            sub = Problem(G * (g1 - g0), g1 - g0, S, D, pb.n_modalities, pb.last_q, pb.block, pb.scale)
+            self.chunks.append(dict(h0=g0 * G, h1=g1 * G, g0=g0, g1=g1,
+                                    sp=SparsePrefill(sub, list(cfgs)[g0 * G:g1 * G], device)))
         self.q = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
         self.k = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
         self.v = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
         self.lab = torch.empty((S,), dtype=torch.uint8, device=device)
         self.o = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
+        self.streams = [torch.cuda.Stream(device=device) for _ in self.chunks]
 
     def h2d_bytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in (self.q, self.k, self.v, self.lab))
@@ -278,10 +294,27 @@ class HostSparsePrefill:
         return self.o.numel() * self.o.element_size()
 
     def __call__(self, q_h, k_h, v_h, lab_h, o_h, stream=None):
-        self.q.copy_(q_h, non_blocking=True)
-        self.k.copy_(k_h, non_blocking=True)
-        self.v.copy_(v_h, non_blocking=True)
-        self.lab.copy_(lab_h, non_blocking=True)
-        self.sp(self.q, self.k, self.v, self.lab, o=self.o, stream=stream)
-        o_h.copy_(self.o, non_blocking=True)
+        caller = stream if stream is not None else torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(caller)
+        for st in self.streams:
+            st.wait_event(start)
+        with torch.cuda.stream(self.streams[0]):
+            self.lab.copy_(lab_h, non_blocking=True)
+            lab_ready = torch.cuda.Event()
+            lab_ready.record(self.streams[0])
+        for i, ch in enumerate(self.chunks):
+            st = self.streams[i % len(self.streams)]
+            st.wait_event(lab_ready)
+            h0, h1, g0, g1 = ch["h0"], ch["h1"], ch["g0"], ch["g1"]
+            with torch.cuda.stream(st):
+                self.q[h0:h1].copy_(q_h[h0:h1], non_blocking=True)
+                self.k[g0:g1].copy_(k_h[g0:g1], non_blocking=True)
+                self.v[g0:g1].copy_(v_h[g0:g1], non_blocking=True)
+                ch["sp"](self.q[h0:h1], self.k[g0:g1], self.v[g0:g1], self.lab, o=self.o[h0:h1], stream=st)
+                o_h[h0:h1].copy_(self.o[h0:h1], non_blocking=True)
+        for st in self.streams:
+            done = torch.cuda.Event()
+            done.record(st)
+            caller.wait_event(done)
         return o_h
