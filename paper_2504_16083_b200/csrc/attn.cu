@@ -97,7 +97,7 @@ struct Smem {
   static constexpr int OFF_KRANK = OFF_KPOS + NKP * BLK * 4;
   static constexpr int OFF_SCHED = OFF_KRANK + NKP * BLK * 4;  // [SCHED_RING] x {idx, pad, WorkItem}: 128 B
   static constexpr int OFF_RI = OFF_SCHED + SCHED_RING * SCHED_ENTRY;     // [2] x {pos[256], rank[256]} of the item's rows
-  // [softmax warp] epilogue staging, 32 rows x EPI_STRIDE each, 512 B aligned (TMA 64B-swizzle atom)
+  // [softmax warp] epilogue staging, 32 rows x EPI_STRIDE each (two 1 KB TMA buffers), 512 B aligned
   static constexpr int OFF_EPI = (OFF_RI + 2 * 2 * 2 * BLK * 4 + 1023) & ~1023;
   static constexpr int OFF_BAR = OFF_EPI + NWARP_SOFT * 32 * EPI_STRIDE;
   // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2][2] p_full[2][2] o_full[2]
@@ -879,18 +879,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const bool fin = (it.out_mode == OUT_FINAL);
       uint32_t ov[D / 2];
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tO + c * 32, r);
+      for (int c = 0; c < D / 32; c += 2) {  // two 32-column loads in flight per wait
+        uint32_t r[2][32];
+        tmem_ld32(tO + c * 32, r[0]);
+        tmem_ld32(tO + c * 32 + 32, r[1]);
         tmem_wait_ld();
-        if (fin) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            ov[c * 16 + j] = pack_bf16(__uint_as_float(r[2 * j]) * inv_l, __uint_as_float(r[2 * j + 1]) * inv_l);
-        } else {
+        for (int h = 0; h < 2; ++h) {
+          if (fin) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            ov[c * 16 + j] = pack_f16(__uint_as_float(r[2 * j]) * inv_l, __uint_as_float(r[2 * j + 1]) * inv_l);
+            for (int j = 0; j < 16; ++j)
+              ov[(c + h) * 16 + j] =
+                  pack_bf16(__uint_as_float(r[h][2 * j]) * inv_l, __uint_as_float(r[h][2 * j + 1]) * inv_l);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              ov[(c + h) * 16 + j] =
+                  pack_f16(__uint_as_float(r[h][2 * j]) * inv_l, __uint_as_float(r[h][2 * j + 1]) * inv_l);
+          }
         }
       }
       tc_fence_before();
@@ -909,29 +915,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int wrow0 = (warp % 4) * 32;  // first row of this warp in the half (its TMEM lane base)
       if (!fin || (!it.q_gathered && __all_sync(0xffffffffu, write))) {
         // The warp's 32 rows are contiguous in the destination (partial rows, or final rows of an
-        // original-order block that are all written): each 32-column chunk is staged in the TMA
-        // 64B-swizzle layout (16 B chunk q of row r at q ^ ((r >> 1) & 3): conflict-free) and written
-        // by one TMA tensor store, asynchronously.
+        // original-order block that are all written): each 16-column chunk (32 rows x 32 B) is
+        // staged in the TMA 32B-swizzle layout (16 B half q of row r at q ^ ((r >> 2) & 1):
+        // conflict-free) in one of two 1 KB buffers and written by one asynchronous TMA tensor
+        // store; a buffer is refilled once the store two chunks back has read it.
         const CUtensorMap* tm = fin ? &tmO : &tmPart;
         const int grow = (fin ? it.q_row0 : it.out_row0) + hf * BLK + wrow0;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          if (c > 0) {
-            if (lane == 0) bulk_wait_read0();  // the previous chunk has left the buffer
+        for (int c = 0; c < D / 16; ++c) {
+          const uint32_t buf = ebuf + (c & 1) * 1024;
+          if (c >= 2) {
+            if (lane == 0) bulk_wait_read1();
             __syncwarp();
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            st_shared_v4(ebuf + lane * 64 + ((q ^ ((lane >> 1) & 3)) * 16), ov[c * 16 + 4 * q],
-                         ov[c * 16 + 4 * q + 1], ov[c * 16 + 4 * q + 2], ov[c * 16 + 4 * q + 3]);
+          for (int q = 0; q < 2; ++q)
+            st_shared_v4(buf + lane * 32 + ((q ^ ((lane >> 2) & 1)) * 16), ov[c * 8 + 4 * q], ov[c * 8 + 4 * q + 1],
+                         ov[c * 8 + 4 * q + 2], ov[c * 8 + 4 * q + 3]);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(tm, ebuf, c * 32, grow);
+            tma_store_2d(tm, buf, c * 16, grow);
             bulk_commit();
           }
         }
-        if (lane == 0) bulk_wait_read0();  // staging buffer free for the next item
+        if (lane == 0) bulk_wait_read0();  // staging buffers free for the next item
         __syncwarp();
       } else {
         // scattered rows: thread-per-row stores would touch 32 rows (32 L1 wavefronts) per
@@ -1022,17 +1030,17 @@ int make_tmap_rows(CUtensorMap* m, const void* base, long long rows, int D) {
   return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
-// rows x D 16-bit row-major output; box = 32 rows x 32 columns (64 B), 64B swizzle (epilogue staging)
+// rows x D 16-bit row-major output; box = 32 rows x 16 columns (32 B), 32B swizzle (epilogue staging)
 static int make_tmap_out(CUtensorMap* m, const void* base, long long rows, int D, CUtensorMapDataType dt) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return -1;
   if (rows <= 0) rows = 1;
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {16, 32};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
