@@ -107,3 +107,17 @@ def test_host_pipeline_matches_device_call(n_chunks):
            torch.from_numpy(np.ascontiguousarray(d["labels"])).pin_memory(), o_h)
         torch.cuda.synchronize()
         assert torch.equal(o_h, ref.cpu())
+
+
+@pytest.mark.parametrize("frames,text", [(0, 1), (0, 50), (0, 127), (0, 129), (1, 44)])
+def test_short_sequences(frames, text):
+    """Degenerate lengths (S = 2 ... 344: a single partial tile, no grid window, fewer rows than
+    last_q): searched-stride Grid (no valid candidate -> reading 'no valid grid candidate'),
+    A-shape, VS and FULL heads still match the oracle."""
+    heads = [HeadConfig.no_boundary(grid(0, True, True, True)), HeadConfig.no_boundary(ashape(16, 32)),
+             HeadConfig.no_boundary(vslash(20, 10)), HeadConfig.no_boundary(full())]
+    wl = small_workload(S_frames=frames, text=text, H=4, Hkv=2, D=64, heads=heads)
+    d = gen_qkv(wl, seed=11)
+    g = run_gpu(wl, d)
+    for h in range(4):
+        _assert_head(check_head(wl, d, g, h))
