@@ -32,7 +32,10 @@
 
 namespace mmi {
 
-constexpr float RESCALE_THRESH = 8.0f;  // lazy rescale: P <= 2^8 (log2 domain)
+#ifndef MMI_RESCALE_THRESH
+#define MMI_RESCALE_THRESH 8.0f
+#endif
+constexpr float RESCALE_THRESH = MMI_RESCALE_THRESH;  // lazy rescale: P <= 2^8 (log2 domain)
 // column pairs (bit i of each group of 8 pairs) whose exp2 runs as a polynomial on the FMA pipe
 // instead of MUFU.EX2: MUFU is 4 lanes/clk per SM sub-partition, so 128 exp2 per row and tile
 // would otherwise take longer than the other half's two MMAs they must hide behind
