@@ -37,10 +37,12 @@ namespace mmi {
 #endif
 constexpr float RESCALE_THRESH = MMI_RESCALE_THRESH;  // lazy rescale: P <= 2^8 (log2 domain)
 // column pairs (bit i of each group of 8 pairs) whose exp2 runs as a polynomial on the FMA pipe
-// instead of MUFU.EX2: MUFU is 4 lanes/clk per SM sub-partition, so 128 exp2 per row and tile
-// would otherwise take longer than the other half's two MMAs they must hide behind
+// instead of MUFU.EX2 (MUFU is 4 lanes/clk per SM sub-partition).  Same-box A/B on the final
+// pipeline: 2/8 -> 1/8 -> 0/8 emulated = 3.706 -> 3.670 -> 3.663 ms (128K), 193.6 -> 171.2 ->
+// 169.7 ms (256K), 67.4 -> 66.0 -> 65.0 ms (1M): the softmax is issue-bound, not MUFU-bound, so
+// every exp2 stays on MUFU (the polynomial remains for experiments)
 #ifndef MMI_EMU_MASK
-#define MMI_EMU_MASK 0x11u
+#define MMI_EMU_MASK 0x00u
 #endif
 constexpr uint32_t EMU_MASK = MMI_EMU_MASK;
 
