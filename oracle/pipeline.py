@@ -12,7 +12,7 @@ from typing import Dict, Optional
 
 import numpy as np
 
-from synth.config import HeadConfig, Problem
+from synth.config import HeadConfig, Problem, KIND_GRID, BND_NONE, BND_K, BND_Q, BND_2D
 from .attention import fingerprint, masked_attention
 from .estimate import estimate_head
 from .masks import head_mask_rows
@@ -53,19 +53,45 @@ def run_head(pb: Problem, cfg: HeadConfig, q_h: np.ndarray, k_g: np.ndarray, v_g
     return dict(index=index, rows=rows, O=O, lse=lse, empty=empty, count=cnt, sumj=sj, sumj2=sj2)
 
 
-def sample_rows(pb: Problem, labels: np.ndarray, index: Dict, seed: int = 0, n_random: int = 512) -> np.ndarray:
-    """Row sample for large S: first/last 128 rows, 8 rows either
-    side of each modality boundary, n_random seeded rows, and the hline rows of a
-    grid index (capped) when present."""
+def hline_rows(boundary: int, index: Dict, labels: np.ndarray, rho: np.ndarray) -> np.ndarray:
+    """Every horizontal-line query row of a head's grid instances (tab:search_space
+    P:755-766), in original positions: No/K-boundary x = p (mod s); Q-boundary rows of
+    modality m with x = p (mod s) (reading C12); 2D rows of modality a whose rank
+    rho = p (mod s) (reading C13)."""
+    S = labels.shape[0]
+    x = np.arange(S)
+    out = []
+    if boundary in (BND_NONE, BND_K):
+        insts = [(index["intra"][0], None, False)]
+    elif boundary == BND_Q:
+        insts = [(inst, m, False) for m, inst in enumerate(index["intra"])]
+    else:
+        insts = [(row[a], a, True) for a, row in enumerate(index["pair"])]
+    for inst, m, ranked in insts:
+        if inst.get("kind") != KIND_GRID or not inst.get("h"):
+            continue
+        coord = rho if ranked else x
+        sel = np.mod(coord, inst["s"]) == inst["p"]
+        if m is not None:
+            sel &= labels == m
+        out.append(x[sel])
+    return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
+
+
+def sample_rows(pb: Problem, labels: np.ndarray, index: Dict, seed: int = 0, n_random: int = 512,
+                boundary: int = BND_NONE, with_hlines: bool = True) -> np.ndarray:
+    """Row sample for large S: the first and last 128 rows, 8 rows
+    either side of EVERY modality boundary, n_random seeded rows and (with_hlines)
+    EVERY horizontal-line row of this head's grid instances."""
     S = labels.shape[0]
     rs = [np.arange(min(128, S)), np.arange(max(0, S - 128), S)]
     b = np.nonzero(labels[1:] != labels[:-1])[0] + 1
-    for x in b[:64]:
-        rs.append(np.arange(max(0, x - 8), min(S, x + 8)))
+    if b.size:
+        rs.append((b[:, None] + np.arange(-8, 8)[None, :]).ravel())
     rng = np.random.default_rng(seed)
     rs.append(rng.integers(0, S, size=n_random))
-    inst = index.get("intra", [None])[0] if index.get("intra") else None
-    if inst is not None and inst.get("kind") == 4 and inst.get("h"):
-        hl = np.arange(inst["p"], S, inst["s"])
-        rs.append(hl[:: max(1, hl.shape[0] // 64)])
-    return np.unique(np.concatenate(rs))
+    if with_hlines:
+        _, rho, _ = modality_groups(labels, pb.n_modalities)
+        rs.append(hline_rows(boundary, index, labels, rho))
+    r = np.unique(np.concatenate(rs))
+    return r[(r >= 0) & (r < S)]

@@ -14,15 +14,12 @@ import torch
 from synth.config import HeadConfig, Problem, grid, ashape, vslash, full, none
 from synth.workloads import build_workload, small_workload, _qwen_heads, GRID_FLAGS
 from synth.gen import gen_qkv
-from gpu_harness import run_gpu, check_head, TOL_MAX, TOL_MEAN
+from gpu_harness import run_gpu, check_head, assert_head
 
 pytestmark = pytest.mark.gpu
 
 
-def _assert_head(res):
-    assert not res["index"]["mismatch"], res
-    assert res["fp_count_ok"] and res["fp_sum_ok"] and res["fp_sum2_ok"], res
-    assert res["max_err"] <= TOL_MAX and res["mean_err"] <= TOL_MEAN, res
+_assert_head = assert_head
 
 
 def test_tiny_config():

@@ -31,15 +31,21 @@ def test_golden_fingerprints(fx):
         labels = np.zeros(S, dtype=np.uint8)
         index = dict(intra=[_inst(fx["pattern"])])
         bnd, nm = BND_NONE, 1
+    elif fx["boundary"] == "q":
+        labels = np.array(fx["labels"], dtype=np.uint8)
+        index = dict(intra=[_inst(p) for p in fx["intra"]])
+        bnd, nm = BND_Q, 2
     else:
         labels = np.array(fx["labels"], dtype=np.uint8)
         index = dict(pair=[[_inst(p) for p in row] for row in fx["pair"]])
         bnd, nm = BND_2D, 2
     _, rho, _ = modality_groups(labels, nm)
     M = head_mask_rows(bnd, index, labels, rho, np.arange(S), S)
-    cnt, sj, _ = fingerprint(M)
+    cnt, sj, sj2 = fingerprint(M)
     assert cnt.tolist() == fx["count"]
     assert [int(x) for x in sj] == fx["sumj"]
+    if "sumj2" in fx:
+        assert [int(x) for x in sj2] == fx["sumj2"]
     # the vectorised builder agrees with the per-element loop
     assert (brute_force_mask(bnd, index, labels, rho, S) == M).all()
 
