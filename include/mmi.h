@@ -14,8 +14,15 @@
  *      lse [H, S] fp32 (natural log of the softmax normaliser), modality [S] u8.
  *  - GQA: query head h reads KV head h / (H / Hkv)  (reading: Qwen2 convention;
  *    the paper is silent).
- *  - All calls are asynchronous on `stream`; none synchronises the device,
- *    allocates or frees, except mmi_export_index (test only: synchronises).
+ *  - All calls are asynchronous on `stream`; none synchronises the device or
+ *    allocates / frees device memory, except the diagnostic calls marked so
+ *    (they synchronise the stream).  The host plan of each distinct (problem,
+ *    cfg_host) is built once and cached with a pinned copy of its device tables
+ *    (small host allocations on first use; up to 16 plans are kept); the tables
+ *    are copied into the workspace by mmi_estimate_index asynchronously.
+ *  - Concurrency: calls on different workspaces may run concurrently on
+ *    different streams / host threads; every piece of mutable device state of a
+ *    call (index, scheduler counter, partial rows) lives in its workspace.
  *  - Scratch and the sparse index live in a caller-provided workspace of at
  *    least mmi_workspace_bytes(problem, cfg_host) bytes (256-byte aligned).  The
  *    same (problem, cfg_host) must be passed to every call of one pass.
@@ -155,6 +162,17 @@ MMI_API mmi_status mmi_export_index(const mmi_problem* problem, const mmi_head_c
 MMI_API mmi_status mmi_sparse_fingerprint(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws,
                                   size_t ws_bytes, const void* q, const void* k, const void* v, int64_t* fp,
                                   mmi_stream_t stream);
+
+/* DIAGNOSTIC (synchronises the stream).  Device-side error flags raised by the last
+ * mmi_estimate_index on this workspace (0 = none):
+ *   MMI_FLAG_LABEL_RANGE  a modality label >= n_modalities: those tokens belong to no
+ *                         modality group, so Q-/2D-boundary heads do not compute their rows;
+ *   MMI_FLAG_SEG_OVERFLOW the index needed more tile segments than the plan's bound: the
+ *                         affected work items were left empty (nothing is written out of bounds). */
+#define MMI_FLAG_LABEL_RANGE 1u
+#define MMI_FLAG_SEG_OVERFLOW 2u
+MMI_API mmi_status mmi_workspace_flags(const mmi_problem* problem, const mmi_head_config* cfg_host, const void* ws,
+                                       size_t ws_bytes, uint32_t* flags_host, mmi_stream_t stream);
 
 /* Thread-local message for the last non-OK status of this thread. */
 MMI_API const char* mmi_last_error(void);

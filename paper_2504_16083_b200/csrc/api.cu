@@ -5,16 +5,17 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
-
-#include <cub/cub.cuh>
 
 #include "../../include/mmi.h"
 #include "estimate.h"
 #include "index.h"
 #include "internal.h"
 #include "plan.h"
+#include "sort.h"
 
 using namespace mmi;
 
@@ -53,20 +54,102 @@ static float tau_of(const mmi_problem* pb) {
   return pb->scale > 0.f ? pb->scale : 1.0f / sqrtf((float)pb->head_dim);
 }
 
-static mmi_status prepare(const mmi_problem* pb, const mmi_head_config* cfg, const void* ws, size_t ws_bytes,
-                          Plan& P, bool need_ws = true) {
+// ---------------------------------------------------------------- plan cache
+// The plan (workspace layout + device tables) is a pure function of (problem, cfg[H]).  It is built
+// once per distinct (problem, cfg) and kept, together with a PINNED host copy of the device-table
+// blob, so that the four calls of a step neither rebuild it nor upload from pageable memory
+// (pageable cudaMemcpyAsync may block the host and is not capturable in a CUDA graph).
+struct CachedPlan {
+  std::string key;
+  Plan P;
+  uint8_t* blob_pinned = nullptr;
+  cudaEvent_t last_upload = nullptr;  // recorded after every upload from blob_pinned
+  uint64_t stamp = 0;
+  ~CachedPlan() {
+    if (last_upload) {
+      cudaEventSynchronize(last_upload);  // the last async copy from blob_pinned has finished
+      cudaEventDestroy(last_upload);
+    }
+    if (blob_pinned) cudaFreeHost(blob_pinned);
+  }
+};
+static std::mutex g_cache_mu;
+static std::vector<std::shared_ptr<CachedPlan>> g_cache;
+static uint64_t g_cache_clock = 0;
+constexpr size_t PLAN_CACHE_CAP = 16;
+
+static std::string plan_key(const mmi_problem* pb, const mmi_head_config* cfg) {
+  std::string k(reinterpret_cast<const char*>(pb), sizeof(mmi_problem));
+  k.append(reinterpret_cast<const char*>(cfg), sizeof(mmi_head_config) * (size_t)pb->n_heads);
+  return k;
+}
+
+static mmi_status get_plan(const mmi_problem* pb, const mmi_head_config* cfg, std::shared_ptr<CachedPlan>& out,
+                           bool need_blob) {
   mmi_status st = check_problem(pb);
   if (st != MMI_OK) return st;
-  std::string err;
-  st = build_plan(pb, cfg, P, err);
-  if (st != MMI_OK) return fail(st, "%s", err.c_str());
-  if (need_ws) {
-    if (!ws) return fail(MMI_E_WORKSPACE, "workspace is NULL");
-    if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(MMI_E_WORKSPACE, "workspace not 256-byte aligned");
-    if (ws_bytes < P.total)
-      return fail(MMI_E_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, P.total);
+  if (!cfg) return fail(MMI_E_INVALID, "cfg_host is NULL");
+  const std::string key = plan_key(pb, cfg);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (auto& e : g_cache)
+      if (e->key == key) {
+        e->stamp = ++g_cache_clock;
+        out = e;
+        if (!need_blob || e->blob_pinned) return MMI_OK;
+        break;
+      }
+  }
+  if (!out) {
+    auto e = std::make_shared<CachedPlan>();
+    std::string err;
+    st = build_plan(pb, cfg, e->P, err);
+    if (st != MMI_OK) return fail(st, "%s", err.c_str());
+    e->key = key;
+    out = e;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (need_blob && !out->blob_pinned) {
+    const std::vector<uint8_t> blob = make_blob(out->P);
+    uint8_t* pin = nullptr;
+    cudaError_t ce = cudaHostAlloc(reinterpret_cast<void**>(&pin), std::max<size_t>(blob.size(), 16), cudaHostAllocDefault);
+    if (ce != cudaSuccess) return fail(MMI_E_CUDA, "cudaHostAlloc(device tables): %s", cudaGetErrorString(ce));
+    memcpy(pin, blob.data(), blob.size());
+    ce = cudaEventCreateWithFlags(&out->last_upload, cudaEventDisableTiming);
+    if (ce != cudaSuccess) {
+      cudaFreeHost(pin);
+      return fail(MMI_E_CUDA, "cudaEventCreate: %s", cudaGetErrorString(ce));
+    }
+    out->blob_pinned = pin;
+  }
+  bool present = false;
+  for (auto& e : g_cache) present |= (e.get() == out.get());
+  if (!present) {
+    if (g_cache.size() >= PLAN_CACHE_CAP) {  // evict the least recently used entry
+      size_t lru = 0;
+      for (size_t i = 1; i < g_cache.size(); ++i)
+        if (g_cache[i]->stamp < g_cache[lru]->stamp) lru = i;
+      g_cache.erase(g_cache.begin() + lru);  // freed when its last user drops it
+    }
+    out->stamp = ++g_cache_clock;
+    g_cache.push_back(out);
   }
   return MMI_OK;
+}
+
+static mmi_status check_ws(const Plan& P, const void* ws, size_t ws_bytes) {
+  if (!ws) return fail(MMI_E_WORKSPACE, "workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(MMI_E_WORKSPACE, "workspace not 256-byte aligned");
+  if (ws_bytes < P.total) return fail(MMI_E_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, P.total);
+  return MMI_OK;
+}
+
+static mmi_status prepare(const mmi_problem* pb, const mmi_head_config* cfg, const void* ws, size_t ws_bytes,
+                          std::shared_ptr<CachedPlan>& cp, bool need_ws = true, bool need_blob = false) {
+  mmi_status st = get_plan(pb, cfg, cp, false);
+  if (st != MMI_OK) return st;
+  if (need_ws && (st = check_ws(cp->P, ws, ws_bytes)) != MMI_OK) return st;
+  return need_blob ? get_plan(pb, cfg, cp, true) : MMI_OK;
 }
 
 template <typename T>
@@ -115,7 +198,9 @@ static IndexCtx make_ctx(const Plan& P, void* ws) {
   C.items_sorted = at<WorkItem>(ws, P.items_sorted);
   C.sort_keys = at<int>(ws, P.item_keys);
   C.sort_vals = at<int>(ws, P.item_vals);
-  C.sort_vals_out = at<int>(ws, P.item_vals) + P.n_slots;
+  C.sort_vals_out = at<int>(ws, P.item_vals);
+  C.seg_cap = P.seg_cap;
+  C.flags = at<unsigned>(ws, P.flags);
   C.part_o = at<__half>(ws, P.part_o);
   C.part_lse = at<float>(ws, P.part_lse);
   return C;
@@ -128,16 +213,17 @@ static IndexCtx make_ctx(const Plan& P, void* ws) {
   } while (0)
 
 extern "C" size_t mmi_workspace_bytes(const mmi_problem* pb, const mmi_head_config* cfg) {
-  Plan P;
-  if (prepare(pb, cfg, nullptr, 0, P, false) != MMI_OK) return 0;
-  return P.total;
+  std::shared_ptr<CachedPlan> cp;
+  if (prepare(pb, cfg, nullptr, 0, cp, false) != MMI_OK) return 0;
+  return cp->P.total;
 }
 
 extern "C" mmi_status mmi_plan_stats(const mmi_problem* pb, const mmi_head_config* cfg, int64_t* out, int n) {
   if (!out || n < 0) return fail(MMI_E_INVALID, "null output");
-  Plan P;
-  const mmi_status st = prepare(pb, cfg, nullptr, 0, P, false);
+  std::shared_ptr<CachedPlan> cp;
+  const mmi_status st = prepare(pb, cfg, nullptr, 0, cp, false);
   if (st != MMI_OK) return st;
+  const Plan& P = cp->P;
   const int64_t v[5] = {P.qg_rows, P.kg_rows, (int64_t)P.merge_heads.size(), (int64_t)P.slabs.size(),
                         (int64_t)P.part_rows};
   for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
@@ -147,16 +233,18 @@ extern "C" mmi_status mmi_plan_stats(const mmi_problem* pb, const mmi_head_confi
 extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_config* cfg, const void* q,
                                          const void* k, const uint8_t* modality, void* ws, size_t ws_bytes,
                                          mmi_stream_t stream) {
-  Plan P;
-  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  std::shared_ptr<CachedPlan> cp;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, cp, true, true);
   if (st != MMI_OK) return st;
+  const Plan& P = cp->P;
   if (!q || !k || !modality) return fail(MMI_E_INVALID, "null tensor pointer");
   cudaStream_t s = (cudaStream_t)stream;
   const int S = P.S;
-  // device tables (pageable source: staged before cudaMemcpyAsync returns)
-  std::vector<uint8_t> blob = make_blob(P);
-  CK(cudaMemcpyAsync(at<char>(ws, P.blob), blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+  // device tables: asynchronous copy from the plan's pinned host blob
+  CK(cudaMemcpyAsync(at<char>(ws, P.blob), cp->blob_pinned, P.blob_bytes, cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(cp->last_upload, s));
   CK(cudaMemcpyAsync(at<uint8_t>(ws, P.labels), modality, S, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemsetAsync(at<char>(ws, P.flags), 0, P.flags.bytes, s));
   // zero the accumulators
   CK(cudaMemsetAsync(at<char>(ws, P.cbuf), 0, P.cbuf.bytes, s));
   CK(cudaMemsetAsync(at<char>(ws, P.dgbuf), 0, P.dgbuf.bytes, s));
@@ -172,7 +260,7 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
   int* chunk_base = chunk_cnt + (size_t)nch * MAX_MOD;
   // a1 modality bookkeeping
   launch_modality(at<uint8_t>(ws, P.labels), S, P.M, P.S_pad, (int)mod_cap, chunk_cnt, chunk_base, info,
-                  at<int>(ws, P.perm), at<int>(ws, P.rank), at<int>(ws, P.modpos), s);
+                  at<int>(ws, P.perm), at<int>(ws, P.rank), at<int>(ws, P.modpos), at<unsigned>(ws, P.flags), s);
   // a2 last_q slab estimation
   int* srows = at<int>(ws, P.slab_rows);
   const size_t ns = std::max<size_t>(P.slabs.size(), 1);
@@ -205,12 +293,11 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
                      (int)P.kview_ids.size(), P.qg_rows, P.kg_rows, s);
   launch_inst_params(C, (int)P.insts.size(), s);
   launch_items_count(C, s);
-  size_t tb = P.scan_tmp_bytes;
-  CK(cub::DeviceScan::ExclusiveSum(at<char>(ws, P.scan_tmp), tb, C.seg_cnt, (int*)C.seg_off, P.n_slots + 1, s));
+  launch_scan_exclusive(C.seg_cnt, (int*)C.seg_off, P.n_slots + 1, at<int>(ws, P.scan_tmp), s);
   launch_items_fill(C, s);
-  tb = P.sort_tmp_bytes;
-  CK(cub::DeviceRadixSort::SortPairsDescending(at<char>(ws, P.sort_tmp), tb, C.sort_keys, C.sort_keys + P.n_slots,
-                                               C.sort_vals, (int*)C.sort_vals_out, P.n_slots, 0, 32, s));
+  // work order: stable ascending sort of the inverted LPT / locality keys (items_fill_kernel)
+  launch_sort_pairs(reinterpret_cast<uint32_t*>(C.sort_keys), reinterpret_cast<uint32_t*>(C.sort_keys) + P.n_slots,
+                    C.sort_vals, C.sort_vals + P.n_slots, P.n_slots, 32, at<int>(ws, P.sort_tmp), s);
   launch_items_gather(C, s);
   CK(cudaGetLastError());
   return MMI_OK;
@@ -218,9 +305,10 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
 
 extern "C" mmi_status mmi_permute(const mmi_problem* pb, const mmi_head_config* cfg, void* ws, size_t ws_bytes,
                                   const void* q, const void* k, const void* v, mmi_stream_t stream) {
-  Plan P;
-  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  std::shared_ptr<CachedPlan> cp;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, cp);
   if (st != MMI_OK) return st;
+  const Plan& P = cp->P;
   if (!q || !k || !v) return fail(MMI_E_INVALID, "null tensor pointer");
   cudaStream_t s = (cudaStream_t)stream;
   launch_gather(at<int>(ws, P.qg_src), P.qg_rows, P.D, q, at<void>(ws, P.qg), nullptr, nullptr, s);
@@ -257,6 +345,7 @@ static mmi_status run_sparse(const Plan& P, const mmi_problem* pb, void* ws, con
   A.fingerprint = fp ? 1 : 0;
   A.dbg = g_dbg;
   A.fp_out = fp;
+  A.sched = at<unsigned int>(ws, P.sched);
   AttnLaunch L;
   L.q = q;
   L.qg = at<void>(ws, P.qg);
@@ -280,9 +369,10 @@ static mmi_status run_sparse(const Plan& P, const mmi_problem* pb, void* ws, con
 extern "C" mmi_status mmi_sparse_prefill(const mmi_problem* pb, const mmi_head_config* cfg, void* ws,
                                          size_t ws_bytes, const void* q, const void* k, const void* v, void* o,
                                          float* lse, mmi_stream_t stream) {
-  Plan P;
-  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  std::shared_ptr<CachedPlan> cp;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, cp);
   if (st != MMI_OK) return st;
+  const Plan& P = cp->P;
   if (!q || !k || !v || !o) return fail(MMI_E_INVALID, "null tensor pointer");
   return run_sparse(P, pb, ws, q, k, v, o, lse, nullptr, (cudaStream_t)stream);
 }
@@ -290,18 +380,20 @@ extern "C" mmi_status mmi_sparse_prefill(const mmi_problem* pb, const mmi_head_c
 extern "C" mmi_status mmi_sparse_fingerprint(const mmi_problem* pb, const mmi_head_config* cfg, void* ws,
                                              size_t ws_bytes, const void* q, const void* k, const void* v,
                                              int64_t* fp, mmi_stream_t stream) {
-  Plan P;
-  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  std::shared_ptr<CachedPlan> cp;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, cp);
   if (st != MMI_OK) return st;
+  const Plan& P = cp->P;
   if (!q || !k || !v || !fp) return fail(MMI_E_INVALID, "null tensor pointer");
   return run_sparse(P, pb, ws, q, k, v, nullptr, nullptr, fp, (cudaStream_t)stream);
 }
 
 extern "C" mmi_status mmi_unpermute(const mmi_problem* pb, const mmi_head_config* cfg, void* ws, size_t ws_bytes,
                                     void* o, float* lse, mmi_stream_t stream) {
-  Plan P;
-  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  std::shared_ptr<CachedPlan> cp;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, cp);
   if (st != MMI_OK) return st;
+  const Plan& P = cp->P;
   if (!o) return fail(MMI_E_INVALID, "null output pointer");
   cudaStream_t s = (cudaStream_t)stream;
   IndexCtx C = make_ctx(P, ws);
@@ -353,9 +445,10 @@ extern "C" mmi_status mmi_dense_prefill(const mmi_problem* pb, const void* q, co
 //   then: items with tiles, total tiles (2 words, int64), segments
 extern "C" mmi_status mmi_traffic_stats(const mmi_problem* pb, const mmi_head_config* cfg, const void* ws,
                                         size_t ws_bytes, int64_t* out, mmi_stream_t stream) {
-  Plan P;
-  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  std::shared_ptr<CachedPlan> cp;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, cp);
   if (st != MMI_OK) return st;
+  const Plan& P = cp->P;
   if (!out) return fail(MMI_E_INVALID, "null output");
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   void* w = const_cast<void*>(ws);
@@ -375,12 +468,24 @@ extern "C" mmi_status mmi_traffic_stats(const mmi_problem* pb, const mmi_head_co
   return MMI_OK;
 }
 
+extern "C" mmi_status mmi_workspace_flags(const mmi_problem* pb, const mmi_head_config* cfg, const void* ws,
+                                          size_t ws_bytes, uint32_t* flags_host, mmi_stream_t stream) {
+  std::shared_ptr<CachedPlan> cp;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, cp);
+  if (st != MMI_OK) return st;
+  if (!flags_host) return fail(MMI_E_INVALID, "flags_host is NULL");
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  CK(cudaMemcpy(flags_host, at<char>(const_cast<void*>(ws), cp->P.flags), sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return MMI_OK;
+}
+
 extern "C" mmi_status mmi_export_index(const mmi_problem* pb, const mmi_head_config* cfg, const void* ws,
                                        size_t ws_bytes, int32_t head, int32_t* host_buf, size_t* words,
                                        mmi_stream_t stream) {
-  Plan P;
-  mmi_status st = prepare(pb, cfg, ws, ws_bytes, P);
+  std::shared_ptr<CachedPlan> cp;
+  mmi_status st = prepare(pb, cfg, ws, ws_bytes, cp);
   if (st != MMI_OK) return st;
+  const Plan& P = cp->P;
   if (head < 0 || head >= P.H) return fail(MMI_E_INVALID, "head out of range");
   if (!words) return fail(MMI_E_INVALID, "words is NULL");
   cudaStream_t s = (cudaStream_t)stream;

@@ -361,7 +361,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int i = 0;; ++i) {
           const int slot = i % SCHED_RING;
           mbar_wait(sched_empty + slot, ((i / SCHED_RING) & 1) ^ 1);
-          int idx = (i == 0) ? (int)blockIdx.x : (int)gridDim.x + (int)atomicAdd(P.sched, 1u);
+          // dynamic fetch from the workspace counter; static round-robin without one (dense
+          // comparator: its implicit items are already in longest-first order)
+          int idx = (i == 0) ? (int)blockIdx.x
+                             : (P.sched ? (int)gridDim.x + (int)atomicAdd(P.sched, 1u) : (int)blockIdx.x + i * (int)gridDim.x);
           if (idx >= n_items) idx = -1;
           sched_ring[slot * (SCHED_ENTRY / 4)] = idx;
           if (idx >= 0 && !P.dense) {
@@ -1050,9 +1053,6 @@ static int make_tmap_out(CUtensorMap* m, const void* base, long long rows, int D
 }
 
 static int g_num_sms = 0;
-// work-item counters for launches without a workspace (dense comparator); rotating slots
-__device__ unsigned int g_sched_counters[64];
-static unsigned g_sched_slot = 0;
 
 cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hint, cudaStream_t stream,
                         int* tmap_err) {
@@ -1072,26 +1072,27 @@ cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hi
   if (e) return cudaErrorInvalidValue;
   if (!g_num_sms) {
     int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t ce = cudaGetDevice(&dev);
+    if (ce == cudaSuccess) ce = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (ce != cudaSuccess) return ce;
   }
   int grid = g_num_sms;
   if (n_items_hint > 0 && (n_items_hint + 1) / 2 < grid) grid = (n_items_hint + 1) / 2;
   if (grid <= 0) return cudaSuccess;
-  AttnParams Pl = P;
-  if (!Pl.sched) {
-    unsigned int* base = nullptr;
-    cudaGetSymbolAddress(reinterpret_cast<void**>(&base), g_sched_counters);
-    Pl.sched = base + (g_sched_slot++ % 64);
+  const AttnParams& Pl = P;
+  if (Pl.sched) {  // the caller's workspace counter, zeroed in stream order before the launch
+    const cudaError_t ce = cudaMemsetAsync(Pl.sched, 0, sizeof(unsigned int), stream);
+    if (ce != cudaSuccess) return ce;
   }
-  cudaMemsetAsync(Pl.sched, 0, sizeof(unsigned int), stream);
   if (P.D == 128) {
     auto kfn = attn_kernel<128>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::ALLOC);
+    const cudaError_t ce = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::ALLOC);
+    if (ce != cudaSuccess) return ce;
     kfn<<<grid, NTHREADS, Smem<128>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], Pl);
   } else {
     auto kfn = attn_kernel<64>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<64>::ALLOC);
+    const cudaError_t ce = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<64>::ALLOC);
+    if (ce != cudaSuccess) return ce;
     kfn<<<grid, NTHREADS, Smem<64>::ALLOC, stream>>>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], Pl);
   }
   return cudaGetLastError();

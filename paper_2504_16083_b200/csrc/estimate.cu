@@ -20,20 +20,24 @@ namespace mmi {
 // =============================================================== a1: modality
 constexpr int MOD_CHUNK = 4096;
 
-__global__ void mod_count_kernel(const uint8_t* __restrict__ labels, int S, int M, int* __restrict__ chunk_cnt) {
+__global__ void mod_count_kernel(const uint8_t* __restrict__ labels, int S, int M, int* __restrict__ chunk_cnt,
+                                 unsigned* __restrict__ flags) {
   __shared__ int cnt[MAX_MOD];
   if (threadIdx.x < MAX_MOD) cnt[threadIdx.x] = 0;
   __syncthreads();
   const int c0 = blockIdx.x * MOD_CHUNK;
   int loc[MAX_MOD] = {0, 0, 0, 0};
+  bool bad = false;
   for (int i = c0 + threadIdx.x; i < min(S, c0 + MOD_CHUNK); i += blockDim.x) {
     const int m = labels[i];
+    bad |= m >= M;
 #pragma unroll
-    for (int q = 0; q < MAX_MOD; ++q) loc[q] += (m == q);
+    for (int q = 0; q < MAX_MOD; ++q) loc[q] += (m == q && q < M);
   }
 #pragma unroll
   for (int q = 0; q < MAX_MOD; ++q)
     if (loc[q]) atomicAdd(&cnt[q], loc[q]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, FLAG_LABEL_RANGE);
   __syncthreads();
   if (threadIdx.x < MAX_MOD) chunk_cnt[blockIdx.x * MAX_MOD + threadIdx.x] = cnt[threadIdx.x];
 }
@@ -64,7 +68,7 @@ __global__ void mod_scan_kernel(const int* __restrict__ chunk_cnt, int n_chunks,
   }
 }
 
-__global__ void mod_place_kernel(const uint8_t* __restrict__ labels, int S, const int* __restrict__ chunk_base,
+__global__ void mod_place_kernel(const uint8_t* __restrict__ labels, int S, int M, const int* __restrict__ chunk_base,
                                  const int* __restrict__ info, int* __restrict__ perm, int* __restrict__ rank,
                                  int* __restrict__ modpos) {
   // 256 threads x 16 consecutive positions = one 4096 chunk
@@ -77,7 +81,7 @@ __global__ void mod_place_kernel(const uint8_t* __restrict__ labels, int S, cons
   for (int i = 0; i < 16; ++i) {
     lab[i] = (c0 + i < S) ? labels[c0 + i] : -1;
 #pragma unroll
-    for (int q = 0; q < MAX_MOD; ++q) loc[q] += (lab[i] == q);
+    for (int q = 0; q < MAX_MOD; ++q) loc[q] += (lab[i] == q && q < M);
   }
   int pre[MAX_MOD];
 #pragma unroll
@@ -90,6 +94,10 @@ __global__ void mod_place_kernel(const uint8_t* __restrict__ labels, int S, cons
   for (int i = 0; i < 16; ++i) {
     const int m = lab[i];
     if (m < 0) continue;
+    if (m >= M) {  // out-of-range label (flagged by mod_count_kernel): in no modality group
+      rank[c0 + i] = 0;
+      continue;
+    }
     int r = 0;
 #pragma unroll
     for (int q = 0; q < MAX_MOD; ++q)
@@ -114,11 +122,11 @@ __global__ void mod_pad_kernel(const int* __restrict__ info, int S, int S_pad, i
 }
 
 void launch_modality(const uint8_t* labels, int S, int M, int S_pad, int mod_cap, int* chunk_cnt, int* chunk_base,
-                     int* info, int* perm, int* rank, int* modpos, cudaStream_t st) {
+                     int* info, int* perm, int* rank, int* modpos, unsigned* flags, cudaStream_t st) {
   const int nch = (S + MOD_CHUNK - 1) / MOD_CHUNK;
-  mod_count_kernel<<<nch, 256, 0, st>>>(labels, S, M, chunk_cnt);
+  mod_count_kernel<<<nch, 256, 0, st>>>(labels, S, M, chunk_cnt, flags);
   mod_scan_kernel<<<1, 32, 0, st>>>(chunk_cnt, nch, M, chunk_base, info);
-  mod_place_kernel<<<nch, 256, 0, st>>>(labels, S, chunk_base, info, perm, rank, modpos);
+  mod_place_kernel<<<nch, 256, 0, st>>>(labels, S, M, chunk_base, info, perm, rank, modpos);
   const int n = max(S_pad, mod_cap);
   mod_pad_kernel<<<(n + 255) / 256, 256, 0, st>>>(info, S, S_pad, mod_cap, rank, modpos);
 }

@@ -15,7 +15,7 @@ constexpr int MI_PADOFF = 9;   // [MAX_MOD+1] offsets of the 128-padded groups i
 constexpr int MI_WORDS = 16;
 
 void launch_modality(const uint8_t* labels, int S, int M, int S_pad, int mod_cap, int* chunk_cnt, int* chunk_base,
-                     int* info, int* perm, int* rank, int* modpos, cudaStream_t st);
+                     int* info, int* perm, int* rank, int* modpos, unsigned* flags, cudaStream_t st);
 void launch_slabs(const DSlab* slabs, int n_slabs, int max_batch, const void* q, const void* k, int S, int H, int Hkv, int D,
                   int last_q, float scale_log2, const int* info, const int* perm, const int* rank,
                   const uint8_t* labels, int* rows, int* rranks, int* sinfo, float2* ml_part, float2* ml, float* cbuf,

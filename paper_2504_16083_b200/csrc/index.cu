@@ -659,9 +659,22 @@ __global__ void items_fill_kernel(IndexCtx C) {
   if (slot >= C.n_slots) return;
   Emitter E;
   const int off = C.seg_off[slot];
-  E.out = C.segs + off;
   E.n_segs = E.n_tiles = 0;
   WorkItem W;
+  if ((int64_t)off + C.seg_cnt[slot] > C.seg_cap) {
+    // the plan's segment bound was short: never write past the region; the item stays empty
+    // (its rows are not computed) and mmi_workspace_flags reports it
+    atomicOr(C.flags, FLAG_SEG_OVERFLOW);
+    E.out = nullptr;
+    build_slot(C, slot, E, W);
+    W.seg_off = off;
+    W.n_segs = W.n_tiles = 0;
+    C.items[slot] = W;
+    C.sort_keys[slot] = ~0;
+    C.sort_vals[slot] = slot;
+    return;
+  }
+  E.out = C.segs + off;
   build_slot(C, slot, E, W);
   W.seg_off = off;
   W.n_segs = E.n_segs;
@@ -669,12 +682,13 @@ __global__ void items_fill_kernel(IndexCtx C) {
   C.items[slot] = W;
   // work order: long items first by length (LPT); short items by position then head,
   // so that concurrently running CTAs share the key tiles of a KV group in L2.
+  // (sorted ascending on the bitwise complement: descending key, equal keys keep slot order)
   int key = 0;
   if (E.n_tiles >= LONG_ITEM_TILES)
     key = 0x40000000 + E.n_tiles;
   else if (E.n_tiles > 0)
     key = 0x3FFFFFFF - ((W.pad[0] / BLK) * 64 + (W.head & 63));
-  C.sort_keys[slot] = key;
+  C.sort_keys[slot] = ~key;
   C.sort_vals[slot] = slot;
 }
 

@@ -37,6 +37,8 @@ struct IndexCtx {
   const int* sort_vals_out;
   const __half* part_o;
   const float* part_lse;
+  int64_t seg_cap;      // capacity of segs (plan bound)
+  unsigned* flags;      // device-side error flags (MMI_FLAG_*)
 };
 
 void launch_build_views(const IndexCtx& C, const int* qviews, int nq, const int* kviews, int nk, int64_t qrows,

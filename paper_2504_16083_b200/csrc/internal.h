@@ -10,6 +10,9 @@ namespace mmi {
 constexpr int BLK = 128;          // row block / key tile (reading C19)
 constexpr int MAX_MOD = 4;
 constexpr int KPAD = 0x7fffffff;  // position of a pad key: never causally visible (reading C14)
+// device-side error flags in the workspace (read back by mmi_workspace_flags)
+constexpr unsigned FLAG_LABEL_RANGE = 1u;   // a modality label >= n_modalities
+constexpr unsigned FLAG_SEG_OVERFLOW = 2u;  // the index needed more tile segments than the plan bound
 
 // ---- segment: a run of consecutive 128-key tiles of one K-view ----
 // meta bits: [0] space (0 = original K/V, 1 = gathered K̄/V̄), [2,5) role,

@@ -1,11 +1,11 @@
 // Host planner: validation of the per-head configs and the workspace layout.
 #include <algorithm>
 #include <cstdio>
+#include <climits>
 #include <cstring>
 
-#include <cub/cub.cuh>
-
 #include "plan.h"
+#include "sort.h"
 
 namespace mmi {
 
@@ -112,8 +112,8 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
     DView v;
     v.kind = kind;
     v.space = space;
-    v.cap = (int32_t)pad128(cap);
-    v.row_off = (int32_t)(space == 0 ? qrow : krow);
+    v.cap = (int32_t)std::min<int64_t>(pad128(cap), INT32_MAX / 2);
+    v.row_off = (int32_t)std::min<int64_t>(space == 0 ? qrow : krow, INT32_MAX / 2);
     v.head = head;
     v.inst = inst;
     v.mod = mod;
@@ -311,17 +311,6 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
   }
   P.n_chunks = (S + SLAB_CHUNK - 1) / SLAB_CHUNK;
 
-  // cub temp sizes
-  {
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, (int*)nullptr, (int*)nullptr, P.n_slots + 1);
-    P.scan_tmp_bytes = tb;
-    tb = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, (int*)nullptr, (int*)nullptr, (int*)nullptr,
-                                              (int*)nullptr, P.n_slots);
-    P.sort_tmp_bytes = tb;
-  }
-
   // ---------------- workspace layout ----------------
   size_t off = 0;
   auto reg = [&](Region& r, size_t bytes) {
@@ -411,15 +400,26 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
   reg(P.items_sorted, sizeof(WorkItem) * P.n_slots);
   reg(P.item_keys, sizeof(int) * 2 * (size_t)P.n_slots);
   reg(P.item_vals, sizeof(int) * 2 * (size_t)P.n_slots);
+  reg(P.sort_tmp, sizeof(int) * sort_hist_ints(P.n_slots));
   reg(P.seg_cnt, sizeof(int) * (P.n_slots + 1));
   reg(P.seg_off, sizeof(int) * (P.n_slots + 1));
   reg(P.segs, sizeof(Seg) * P.seg_cap);
   reg(P.inst_params, sizeof(InstParam) * P.insts.size());
-  reg(P.sort_tmp, P.sort_tmp_bytes);
-  reg(P.scan_tmp, P.scan_tmp_bytes);
+  reg(P.scan_tmp, sizeof(int) * scan_tmp_ints(P.n_slots + 1));
+  reg(P.sched, 256);   // attention work-item counter (zeroed on the call's stream before each launch)
+  reg(P.flags, 256);   // device-side error flags (mmi_workspace_flags)
   reg(P.part_o, sizeof(uint16_t) * (size_t)std::max<int64_t>(P.part_rows, 1) * P.D);  // fp16
   reg(P.part_lse, sizeof(float) * (size_t)std::max<int64_t>(P.part_rows, 1));
   P.total = off;
+  // 32-bit row / segment indexing inside the kernels (WorkItem.q_row0, DView.row_off, Seg.krow0)
+  const int64_t lim = (int64_t)1 << 31;
+  int64_t worst = std::max<int64_t>({P.qg_rows, P.kg_rows, P.part_rows, P.seg_cap, (int64_t)P.n_slots + 1,
+                                     (int64_t)P.Hkv * P.S + BLK, (int64_t)P.H * P.S + BLK});
+  for (const DView& v : P.views) worst = std::max<int64_t>(worst, (int64_t)v.row_off + v.cap);
+  if (worst >= lim) {
+    err = "plan needs " + std::to_string(worst) + " rows / segments: exceeds 32-bit indexing";
+    return MMI_E_UNSUPPORTED;
+  }
   return MMI_OK;
 }
 

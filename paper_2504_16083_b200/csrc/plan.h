@@ -108,8 +108,8 @@ struct Plan {
   Region qg_pos, qg_rank, qg_src, kg_pos, kg_rank, kg_src, qg, kg, vg;
   Region items, item_keys, item_vals, items_sorted, seg_cnt, seg_off, segs, inst_params, sort_tmp, scan_tmp;
   Region part_o, part_lse;
+  Region sched, flags;
   size_t total = 0;
-  size_t sort_tmp_bytes = 0, scan_tmp_bytes = 0;
 };
 
 // Builds the plan; returns MMI_OK or an error status with message in `err`.

@@ -70,11 +70,12 @@ def lib():
         L.mmi_sparse_fingerprint.argtypes = [P, C, vp, sz, vp, vp, vp, vp, vp]
         L.mmi_plan_stats.argtypes = [P, C, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         L.mmi_traffic_stats.argtypes = [P, C, vp, sz, ctypes.POINTER(ctypes.c_int64), vp]
+        L.mmi_workspace_flags.argtypes = [P, C, vp, sz, ctypes.POINTER(ctypes.c_uint32), vp]
         L.mmi_last_error.restype = ctypes.c_char_p
         L.mmi_version.restype = ctypes.c_char_p
         for fn in ("mmi_estimate_index", "mmi_permute", "mmi_sparse_prefill", "mmi_unpermute",
                    "mmi_dense_prefill", "mmi_export_index", "mmi_sparse_fingerprint", "mmi_plan_stats",
-                   "mmi_traffic_stats"):
+                   "mmi_traffic_stats", "mmi_workspace_flags"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -127,6 +128,26 @@ def _need_cuda(*ts):
             raise ValueError("mmi: contiguous CUDA tensors required")
 
 
+def _check_tensor(name, t, dtype, shape):
+    """The C ABI reads raw pointers: dtype and shape are checked here (include/mmi.h layouts)."""
+    if t is None:
+        return
+    if t.dtype != dtype:
+        raise TypeError(f"mmi: {name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"mmi: {name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+def _check_io(pb: Problem, q=None, k=None, v=None, modality=None, o=None, lse=None):
+    H, Hkv, S, D = pb.n_heads, pb.n_kv_heads, pb.seq_len, pb.head_dim
+    _check_tensor("q", q, torch.bfloat16, (H, S, D))
+    _check_tensor("k", k, torch.bfloat16, (Hkv, S, D))
+    _check_tensor("v", v, torch.bfloat16, (Hkv, S, D))
+    _check_tensor("modality", modality, torch.uint8, (S,))
+    _check_tensor("o", o, torch.bfloat16, (H, S, D))
+    _check_tensor("lse", lse, torch.float32, (H, S))
+
+
 # ------------------------------------------------------------------ C ABI mirrors
 def mmi_workspace_bytes(pb: Problem, cfgs: Sequence[HeadConfig]) -> int:
     return int(lib().mmi_workspace_bytes(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs)))
@@ -149,18 +170,21 @@ def mmi_traffic_stats(pb: Problem, cfgs: Sequence[HeadConfig], ws, stream=None) 
 
 def mmi_estimate_index(pb, cfgs, q, k, modality, ws, stream=None):
     _need_cuda(q, k, modality, ws)
+    _check_io(pb, q=q, k=k, modality=modality)
     _check(lib().mmi_estimate_index(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(q), _ptr(k),
                                     _ptr(modality), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def mmi_permute(pb, cfgs, ws, q, k, v, stream=None):
     _need_cuda(q, k, v, ws)
+    _check_io(pb, q=q, k=k, v=v)
     _check(lib().mmi_permute(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
                              ws.numel() * ws.element_size(), _ptr(q), _ptr(k), _ptr(v), _stream(stream)))
 
 
 def mmi_sparse_prefill(pb, cfgs, ws, q, k, v, o, lse=None, stream=None):
     _need_cuda(q, k, v, o, ws, lse)
+    _check_io(pb, q=q, k=k, v=v, o=o, lse=lse)
     _check(lib().mmi_sparse_prefill(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
                                     ws.numel() * ws.element_size(), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
                                     _stream(stream)))
@@ -168,12 +192,14 @@ def mmi_sparse_prefill(pb, cfgs, ws, q, k, v, o, lse=None, stream=None):
 
 def mmi_unpermute(pb, cfgs, ws, o, lse=None, stream=None):
     _need_cuda(o, ws, lse)
+    _check_io(pb, o=o, lse=lse)
     _check(lib().mmi_unpermute(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
                                ws.numel() * ws.element_size(), _ptr(o), _ptr(lse), _stream(stream)))
 
 
 def mmi_dense_prefill(pb, q, k, v, o, lse=None, stream=None):
     _need_cuda(q, k, v, o, lse)
+    _check_io(pb, q=q, k=k, v=v, o=o, lse=lse)
     _check(lib().mmi_dense_prefill(ctypes.byref(to_c_problem(pb)), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
                                    _stream(stream)))
 
@@ -183,6 +209,15 @@ def mmi_sparse_fingerprint(pb, cfgs, ws, q, k, v, fp, stream=None):
     _check(lib().mmi_sparse_fingerprint(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
                                         ws.numel() * ws.element_size(), _ptr(q), _ptr(k), _ptr(v), _ptr(fp),
                                         _stream(stream)))
+
+
+def mmi_workspace_flags(pb, cfgs, ws, stream=None) -> int:
+    """DIAGNOSTIC (synchronises): device-side error flags of the last estimate on ws
+    (1 = a modality label >= n_modalities, 2 = segment-bound overflow)."""
+    f = ctypes.c_uint32(0)
+    _check(lib().mmi_workspace_flags(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
+                                     ws.numel() * ws.element_size(), ctypes.byref(f), _stream(stream)))
+    return int(f.value)
 
 
 def mmi_export_index(pb, cfgs, ws, head: int, stream=None) -> torch.Tensor:
@@ -214,18 +249,26 @@ class SparsePrefill:
         self.ws_bytes = nbytes
 
     def estimate(self, q, k, modality, stream=None):
+        _need_cuda(q, k, modality)
+        _check_io(self.pb, q=q, k=k, modality=modality)
         _check(lib().mmi_estimate_index(ctypes.byref(self.c_pb), self.c_cfg, _ptr(q), _ptr(k), _ptr(modality),
                                         _ptr(self.ws), self.ws_bytes, _stream(stream)))
 
     def permute(self, q, k, v, stream=None):
+        _need_cuda(q, k, v)
+        _check_io(self.pb, q=q, k=k, v=v)
         _check(lib().mmi_permute(ctypes.byref(self.c_pb), self.c_cfg, _ptr(self.ws), self.ws_bytes, _ptr(q), _ptr(k),
                                  _ptr(v), _stream(stream)))
 
     def sparse(self, q, k, v, o, lse=None, stream=None):
+        _need_cuda(q, k, v, o, lse)
+        _check_io(self.pb, q=q, k=k, v=v, o=o, lse=lse)
         _check(lib().mmi_sparse_prefill(ctypes.byref(self.c_pb), self.c_cfg, _ptr(self.ws), self.ws_bytes, _ptr(q),
                                         _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _stream(stream)))
 
     def unpermute(self, o, lse=None, stream=None):
+        _need_cuda(o, lse)
+        _check_io(self.pb, o=o, lse=lse)
         _check(lib().mmi_unpermute(ctypes.byref(self.c_pb), self.c_cfg, _ptr(self.ws), self.ws_bytes, _ptr(o),
                                    _ptr(lse), _stream(stream)))
 
@@ -240,14 +283,22 @@ class SparsePrefill:
         self.unpermute(o, lse, stream)
         return o
 
-    def total_tiles(self) -> int:
-        """Computed key tiles of the last index (TEST/bench helper: synchronises)."""
+    def flags(self, stream=None) -> int:
+        """DIAGNOSTIC (synchronises): device-side error flags of the last estimate."""
+        return mmi_workspace_flags(self.pb, self.cfgs, self.ws, stream)
+
+    def head_tiles(self) -> List[int]:
+        """Computed 128x128 key tiles per head of the last index (bench helper: synchronises)."""
         import struct
-        t = 0
+        out = []
         for h in range(self.pb.n_heads):
             w = mmi_export_index(self.pb, self.cfgs, self.ws, h).tolist()
-            t += struct.unpack("<q", struct.pack("<ii", w[-3], w[-2]))[0]
-        return t
+            out.append(struct.unpack("<q", struct.pack("<ii", w[-3], w[-2]))[0])
+        return out
+
+    def total_tiles(self) -> int:
+        """Computed key tiles of the last index (TEST/bench helper: synchronises)."""
+        return sum(self.head_tiles())
 
 
 def dense_prefill(pb: Problem, q, k, v, o=None, lse=None, stream=None):

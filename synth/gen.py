@@ -14,6 +14,8 @@ The planted truth (stride, phase) is returned beside the tensors.
 """
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
 from typing import Dict
 
 import numpy as np
@@ -71,7 +73,10 @@ def _head_role(cfg) -> Dict[str, object]:
 
 
 def gen_qkv(wl: Workload, seed: int = 0, chunk: int = 1 << 16,
-            dtype=torch.bfloat16) -> Dict[str, object]:
+            dtype=torch.bfloat16, only_heads=None) -> Dict[str, object]:
+    """only_heads: generate Q for these heads and K/V for their KV groups only (the other
+    entries stay zero); the generated values are bit-identical to a full call, since every
+    head and group draws from its own SeedSequence stream."""
     pb = wl.problem
     H, Hkv, S, D = pb.n_heads, pb.n_kv_heads, pb.seq_len, pb.head_dim
     G = H // Hkv
@@ -85,16 +90,16 @@ def gen_qkv(wl: Workload, seed: int = 0, chunk: int = 1 << 16,
     kv_seeds = ss.spawn(Hkv)
     q_seeds = ss.spawn(H)
 
-    q = torch.empty((H, S, D), dtype=dtype)
-    k = torch.empty((Hkv, S, D), dtype=dtype)
-    v = torch.empty((Hkv, S, D), dtype=dtype)
+    alloc = torch.empty if only_heads is None else torch.zeros
+    q = alloc((H, S, D), dtype=dtype)
+    k = alloc((Hkv, S, D), dtype=dtype)
+    v = alloc((Hkv, S, D), dtype=dtype)
 
     pos = np.arange(S)
     is_vis = labels == VISION
     freqs = 2 * np.pi / np.array([61.0, 157.0])   # short periods, coprime, far from 2^k strides
 
-    groups = []
-    for g in range(Hkv):
+    def make_group(g):
         rng = np.random.default_rng(kv_seeds[g])
         phi = _unit(rng, TPF, D)
         # 0:g1 1:g2 2:sink 3:vs 4..7 locality basis; orthonormal so that one
@@ -109,7 +114,6 @@ def gen_qkv(wl: Workload, seed: int = 0, chunk: int = 1 << 16,
         p_g2 = int(rng.integers(0, s_g2))
         vs_keys = rng.random(S) < (1.0 / 400.0)
         vs_keys[:4] = False
-        groups.append(dict(phi=phi, u=u, x_g1=x_g1, s_g2=s_g2, p_g2=p_g2, vs_keys=vs_keys))
         for c0 in range(0, S, chunk):
             c1 = min(S, c0 + chunk)
             n = c1 - c0
@@ -128,9 +132,17 @@ def gen_qkv(wl: Workload, seed: int = 0, chunk: int = 1 << 16,
                 kk += a * (np.outer(np.cos(w * pc), u[4 + 2 * f]) + np.outer(np.sin(w * pc), u[5 + 2 * f]))
             k[g, c0:c1] = torch.from_numpy(kk.astype(np.float32)).to(dtype)
             v[g, c0:c1] = torch.from_numpy(rng.standard_normal((n, D)).astype(np.float32)).to(dtype)
+        return dict(phi=phi, u=u, x_g1=x_g1, s_g2=s_g2, p_g2=p_g2, vs_keys=vs_keys)
 
-    planted = []
-    for h in range(H):
+    # every KV group / query head draws from its own SeedSequence stream, so the groups and heads
+    # are generated in parallel threads (numpy RNG and BLAS release the GIL) with a result that is
+    # bit-identical to a sequential loop
+    with ThreadPoolExecutor(max_workers=max(1, min(os.cpu_count() or 1, 32))) as ex:
+        need_g = sorted({h // G for h in (only_heads if only_heads is not None else range(H))})
+        made = dict(zip(need_g, ex.map(make_group, need_g)))
+    groups = [made.get(g) for g in range(Hkv)]
+
+    def make_head(h):
         g = h // G
         gr = groups[g]
         u, phi = gr["u"], gr["phi"]
@@ -154,7 +166,6 @@ def gen_qkv(wl: Workload, seed: int = 0, chunk: int = 1 << 16,
             elif p.kind == KIND_VSLASH:
                 d += u[3]
             dirs[lab] = d
-        planted.append(info)
         for c0 in range(0, S, chunk):
             c1 = min(S, c0 + chunk)
             n = c1 - c0
@@ -173,5 +184,11 @@ def gen_qkv(wl: Workload, seed: int = 0, chunk: int = 1 << 16,
                 a = (G_LOCAL / len(freqs)) ** 0.5 * scale_dir
                 qq += a * (np.outer(np.cos(w * pc), u[4 + 2 * f]) + np.outer(np.sin(w * pc), u[5 + 2 * f]))
             q[h, c0:c1] = torch.from_numpy(qq.astype(np.float32)).to(dtype)
+        return info
+
+    with ThreadPoolExecutor(max_workers=max(1, min(os.cpu_count() or 1, 32))) as ex:
+        hs = list(only_heads) if only_heads is not None else list(range(H))
+        made_h = dict(zip(hs, ex.map(make_head, hs)))
+    planted = [made_h.get(h, {}) for h in range(H)]
 
     return dict(q=q, k=k, v=v, labels=labels, planted=planted, vision_rank=vr)

@@ -127,3 +127,41 @@ def test_plan_stats_rejects_invalid():
                               out, 5)
     assert st != 0
     assert lib().mmi_plan_stats(None, None, out, 5) != 0
+
+
+def test_binding_checks_dtype_and_shape():
+    """The binding checks dtype / shape before handing raw pointers to the C ABI."""
+    import torch
+    from paper_2504_16083_b200.mmi import _check_io
+    pb = Problem(4, 2, 300, 64)
+    ok = dict(q=torch.zeros(4, 300, 64, dtype=torch.bfloat16), k=torch.zeros(2, 300, 64, dtype=torch.bfloat16),
+              v=torch.zeros(2, 300, 64, dtype=torch.bfloat16), modality=torch.zeros(300, dtype=torch.uint8),
+              o=torch.zeros(4, 300, 64, dtype=torch.bfloat16), lse=torch.zeros(4, 300))
+    _check_io(pb, **ok)
+    bad = [("q", torch.zeros(4, 300, 64, dtype=torch.float16)), ("q", torch.zeros(300, 4, 64, dtype=torch.bfloat16)),
+           ("k", torch.zeros(4, 300, 64, dtype=torch.bfloat16)), ("modality", torch.zeros(300, dtype=torch.int64)),
+           ("lse", torch.zeros(4, 300, dtype=torch.float64)), ("o", torch.zeros(4, 300, 128, dtype=torch.bfloat16))]
+    for name, t in bad:
+        with pytest.raises((TypeError, ValueError)):
+            _check_io(pb, **dict(ok, **{name: t}))
+
+
+def test_plan_rejects_32bit_overflow():
+    """A config whose gathered spaces exceed 32-bit row indexing is rejected on the host."""
+    # many searched-stride grid heads with slash lines at the largest S that passes check_problem
+    pb = Problem(16, 16, (1 << 26) - 1024, 128)   # (S + 512) * H <= 2^30 passes check_problem
+    heads = [HeadConfig.no_boundary(grid(0, True, True, True, stride_min=1, stride_max=1024))] * 16
+    assert _ws(pb, heads) == 0
+    from paper_2504_16083_b200.mmi import lib
+    assert b"32-bit" in lib().mmi_last_error()
+
+
+def test_plan_cache_is_stable():
+    """The cached plan (built once per distinct config) gives the same sizes as a fresh one."""
+    wl = build_workload(1)
+    a = _ws(wl.problem, wl.heads)
+    for _ in range(3):
+        assert _ws(wl.problem, wl.heads) == a
+    for i in range(20):   # more distinct configs than the cache keeps: eviction path
+        assert _ws(Problem(1, 1, 1000 + i, 64), [HeadConfig.no_boundary(full())]) > 0
+    assert _ws(wl.problem, wl.heads) == a

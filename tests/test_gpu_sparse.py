@@ -118,3 +118,50 @@ def test_short_sequences(frames, text):
     g = run_gpu(wl, d)
     for h in range(4):
         _assert_head(check_head(wl, d, g, h))
+
+
+def test_concurrent_instances_on_two_streams():
+    """Two SparsePrefill instances (own workspaces) running concurrently on two streams give
+    outputs bit-identical to running them one after the other: every piece of mutable device
+    state (index, scheduler counter, partial rows) lives in the caller's workspace."""
+    import paper_2504_16083_b200 as mmi
+    heads = _mixed_no_boundary_heads()[:8]
+    wl = small_workload(S_frames=24, text=100, H=8, Hkv=4, D=128, heads=heads)
+    d = gen_qkv(wl, seed=13)
+    d2 = gen_qkv(wl, seed=14)
+    pb = wl.problem
+    lab = torch.from_numpy(np.ascontiguousarray(d["labels"])).cuda()
+    ins = [(d["q"].cuda(), d["k"].cuda(), d["v"].cuda()), (d2["q"].cuda(), d2["k"].cuda(), d2["v"].cuda())]
+    sps = [mmi.SparsePrefill(pb, wl.heads), mmi.SparsePrefill(pb, wl.heads)]
+    ref = [sps[i](*ins[i], lab).clone() for i in range(2)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty_like(ref[0]) for _ in range(2)]
+    for rep in range(5):
+        for i in range(2):
+            with torch.cuda.stream(streams[i]):
+                sps[i](*ins[i], lab, o=outs[i], stream=streams[i])
+        torch.cuda.synchronize()
+        for i in range(2):
+            assert torch.equal(outs[i], ref[i]), (rep, i)
+
+
+def test_label_out_of_range_flag():
+    """Labels >= n_modalities are reported by the device-side flag (no out-of-bounds writes)."""
+    import paper_2504_16083_b200 as mmi
+    heads = [HeadConfig.q_boundary([grid(256, True, True, False), vslash(100, 64)])] * 2
+    wl = small_workload(S_frames=3, interleave=2, text_len=200, H=2, Hkv=1, D=64, heads=heads)
+    d = gen_qkv(wl, seed=15)
+    pb = wl.problem
+    sp = mmi.SparsePrefill(pb, wl.heads)
+    lab = torch.from_numpy(np.ascontiguousarray(d["labels"])).cuda()
+    q, k, v = d["q"].cuda(), d["k"].cuda(), d["v"].cuda()
+    sp(q, k, v, lab)
+    assert sp.flags() == 0
+    bad = lab.clone()
+    bad[5] = 3
+    bad[100] = 200
+    sp(q, k, v, bad)
+    assert sp.flags() & 1
+    sp(q, k, v, lab)
+    assert sp.flags() == 0
