@@ -59,8 +59,14 @@ typedef enum {
   MMI_E_CUDA = 6         /* a CUDA launch / tensor-map creation failed             */
 } mmi_status;
 
-/* Pattern kinds ("A-shape, Vertical-Slash and Grid" + FULL / NONE). */
-typedef enum { MMI_PAT_NONE = 0, MMI_PAT_FULL = 1, MMI_PAT_ASHAPE = 2, MMI_PAT_VSLASH = 3, MMI_PAT_GRID = 4 } mmi_kind;
+/* Pattern kinds ("A-shape, Vertical-Slash and Grid" + FULL / NONE) and the static
+ * baseline patterns of the paper's evaluation (tab:impl_details P:685-688). */
+typedef enum {
+  MMI_PAT_NONE = 0, MMI_PAT_FULL = 1, MMI_PAT_ASHAPE = 2, MMI_PAT_VSLASH = 3, MMI_PAT_GRID = 4,
+  MMI_PAT_TRISHAPE = 5,   /* y < sink or x - y < local or x >= S - bottom   (No/K-boundary heads only) */
+  MMI_PAT_SF_FIXED = 6,   /* floor(y / local) == floor(x / local) or y = 0 (mod stride)  (reading C23) */
+  MMI_PAT_SF_STRIDED = 7  /* x - y < local or (x - y) = 0 (mod stride)                   (reading C23) */
+} mmi_kind;
 /* Boundary types. K-boundary executes as No-boundary. */
 typedef enum { MMI_BND_NONE = 0, MMI_BND_K = 1, MMI_BND_Q = 2, MMI_BND_2D = 3 } mmi_boundary;
 
@@ -77,8 +83,9 @@ typedef struct {
   int32_t kind;
   int32_t sink, local;
   int32_t n_vertical, n_slash;
-  int32_t stride, stride_min, stride_max;
+  int32_t stride, stride_min, stride_max;   /* SF_*: stride (1..1024) of the vertical / dilated lines */
   uint8_t use_hline, use_vline, use_slash, _pad;
+  int32_t bottom;                           /* TRISHAPE: dense query rows at the end (>= 0) */
 } mmi_pattern;
 
 #define MMI_MAX_MOD 4

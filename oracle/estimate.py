@@ -27,6 +27,7 @@ from typing import Dict, List, Optional
 import numpy as np
 
 from synth.config import (KIND_NONE, KIND_FULL, KIND_ASHAPE, KIND_VSLASH, KIND_GRID,
+                          KIND_TRISHAPE, KIND_SF_FIXED, KIND_SF_STRIDED,
                           BND_NONE, BND_K, BND_Q, BND_2D, Pattern, HeadConfig, Problem)
 from .modality import modality_groups
 
@@ -155,11 +156,16 @@ def grid_candidates(p: Pattern) -> List[int]:
     return list(range(max(1, p.stride_min), p.stride_max + 1))
 
 
-def _instance(p: Pattern, c, dg, jmax, omax, w_lo, w_hi, key_set=None, force=True) -> Dict:
+def _instance(p: Pattern, c, dg, jmax, omax, w_lo, w_hi, key_set=None, force=True, n=0) -> Dict:
+    """n: extent of the pattern's coordinate system (rows of the head / of the modality)."""
     if p.kind in (KIND_NONE, KIND_FULL):
         return dict(kind=p.kind)
     if p.kind == KIND_ASHAPE:
         return dict(kind=p.kind, sink=p.sink, local=p.local)
+    if p.kind == KIND_TRISHAPE:   # static (P:452): no estimation
+        return dict(kind=p.kind, sink=p.sink, local=p.local, bottom=p.bottom, n=n)
+    if p.kind in (KIND_SF_FIXED, KIND_SF_STRIDED):   # static (P:450-451)
+        return dict(kind=p.kind, local=p.local, stride=p.stride)
     if p.kind == KIND_VSLASH:
         d = select_vs(c, dg, p.n_vertical, p.n_slash, jmax, omax, force=force, key_set=key_set)
         d["kind"] = p.kind
@@ -189,7 +195,7 @@ def estimate_head(pb: Problem, cfg: HeadConfig, q_h: np.ndarray, k_g: np.ndarray
             c, dg = column_mass(A), diagonal_mass(A, R)
         out["slab"] = [R]
         out["intra"] = [_instance(p, c, dg, int(R.max()), int(R.max()),
-                                  FOLD_LO, int(R.min()) - FOLD_GAP)]
+                                  FOLD_LO, int(R.min()) - FOLD_GAP, n=S)]
         out["c"], out["dg"] = [c], [dg]
         return out
     if cfg.boundary == BND_Q:
@@ -206,7 +212,7 @@ def estimate_head(pb: Problem, cfg: HeadConfig, q_h: np.ndarray, k_g: np.ndarray
                 A = slab_attention(q_h[R], k_g, R, tau)
                 c, dg = column_mass(A), diagonal_mass(A, R)
             out["intra"].append(_instance(p, c, dg, int(R.max()), int(R.max()),
-                                          FOLD_LO, int(R.min()) - FOLD_GAP))
+                                          FOLD_LO, int(R.min()) - FOLD_GAP, n=S))
             out["slab"].append(R); out["c"].append(c); out["dg"].append(dg)
         return out
     if cfg.boundary == BND_2D:
@@ -233,7 +239,7 @@ def estimate_head(pb: Problem, cfg: HeadConfig, q_h: np.ndarray, k_g: np.ndarray
                         out["c"][a], out["dg"][a] = ca, dga
                     rR = rho[R]
                     out["pair"][a][a] = _instance(p, ca, dga, int(rR.max()), int(rR.max()),
-                                                  FOLD_LO, int(rR.min()) - FOLD_GAP)
+                                                  FOLD_LO, int(rR.min()) - FOLD_GAP, n=int(P[a].size))
                 else:
                     out["pair"][a][b] = _instance(p, c_full, None, int(R.max()), 0, 0, 0,
                                                   key_set=P[b], force=False)

@@ -14,6 +14,15 @@ intersected with causality y <= x by the caller):
         or (sl and x - y = 0 mod s)
         ("horizontal and vertical lines are evenly spaced and often
          symmetrical"; tab:search_space flags P:755-766; C8 sink/local)
+  TRISHAPE(sink, local, bottom) over n rows
+                            y < sink  or  x - y < local  or  x >= n - bottom
+        (P:452 "full attention for all tokens to the last window's queries";
+         tab:impl_details P:688 Sink 128, Local 4096, Bottom 128)
+  SF_FIXED(l, stride)       floor(y / l) = floor(x / l)  or  y = 0 mod stride
+        (P:450 "attention within each segment ... the segment's initial tokens";
+         P:686 Local = vline_stride = token_per_frame; reading C23)
+  SF_STRIDED(l, stride)     x - y < l  or  (x - y) = 0 mod stride
+        ("local windows with dilated attention"; reading C23)
 Boundary application (readings C12, C13):
   No/K-boundary  M(i,j) = A_P(i, j) with the global index
   Q-boundary     M(i,j) = A_{intra[lab(i)]}(i, j)          (original coordinates)
@@ -28,6 +37,7 @@ from typing import Dict
 import numpy as np
 
 from synth.config import (KIND_NONE, KIND_FULL, KIND_ASHAPE, KIND_VSLASH, KIND_GRID,
+                          KIND_TRISHAPE, KIND_SF_FIXED, KIND_SF_STRIDED,
                           BND_NONE, BND_K, BND_Q, BND_2D)
 
 
@@ -63,6 +73,15 @@ def pattern_pred(inst: Dict, x: np.ndarray, y: np.ndarray) -> np.ndarray:
             m = m | (np.mod(y, s) == p)
         if inst["sl"]:
             m = m | (np.mod(x - y, s) == 0)
+        return np.broadcast_to(m, shape)
+    if kind == KIND_TRISHAPE:
+        m = (y < inst["sink"]) | ((x - y) < inst["local"]) | (x >= inst["n"] - inst["bottom"])
+        return np.broadcast_to(m, shape)
+    if kind == KIND_SF_FIXED:
+        m = (np.floor_divide(y, inst["local"]) == np.floor_divide(x, inst["local"])) | (np.mod(y, inst["stride"]) == 0)
+        return np.broadcast_to(m, shape)
+    if kind == KIND_SF_STRIDED:
+        m = ((x - y) < inst["local"]) | (np.mod(x - y, inst["stride"]) == 0)
         return np.broadcast_to(m, shape)
     raise ValueError(f"unknown pattern kind {kind}")
 
@@ -124,6 +143,12 @@ def brute_force_mask(boundary: int, index: Dict, labels, rho, S: int) -> np.ndar
             s, p = inst["s"], inst["p"]
             return (y < inst["sink"] or x - y < inst["local"] or (inst["h"] and x % s == p)
                     or (inst["v"] and y % s == p) or (inst["sl"] and (x - y) % s == 0))
+        if k == KIND_TRISHAPE:
+            return y < inst["sink"] or x - y < inst["local"] or x >= inst["n"] - inst["bottom"]
+        if k == KIND_SF_FIXED:
+            return y // inst["local"] == x // inst["local"] or y % inst["stride"] == 0
+        if k == KIND_SF_STRIDED:
+            return x - y < inst["local"] or (x - y) % inst["stride"] == 0
         raise ValueError(k)
 
     M = np.zeros((S, S), dtype=bool)

@@ -251,7 +251,6 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
   CK(cudaMemsetAsync(at<char>(ws, P.bits), 0, P.bits.bytes, s));
   CK(cudaMemsetAsync(at<char>(ws, P.vs_cnt), 0, P.vs_cnt.bytes, s));
   CK(cudaMemsetAsync(at<char>(ws, P.seg_cnt), 0, P.seg_cnt.bytes, s));
-  CK(cudaMemsetAsync(at<char>(ws, P.grid_acc), 0, P.grid_acc.bytes, s));
   const int64_t mod_cap = (P.S + (int64_t)P.M * BLK + BLK - 1) / BLK * BLK;
   IndexCtx C = make_ctx(P, ws);
   int* info = at<int>(ws, P.mod_cnt);
@@ -267,22 +266,18 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
   int* srank = srows + ns * SLAB_ROWS;
   int* sinfo = srank + ns * SLAB_ROWS;
   const DSlab* dslabs = blob_at<DSlab>(ws, P, P.o_slabs);
-  int max_batch = 1;
-  {
-    std::vector<int> per_kv(P.Hkv, 0);
-    for (const auto& sl : P.slabs) per_kv[sl.kv]++;
-    for (int c : per_kv) max_batch = std::max(max_batch, (c + 3) / 4);
-  }
-  launch_slabs(dslabs, (int)P.slabs.size(), max_batch, q, k, S, P.H, P.Hkv, P.D, P.pb.last_q, tau_of(pb) * 1.4426950408889634f,
-               info, at<int>(ws, P.perm), at<int>(ws, P.rank), at<uint8_t>(ws, P.labels), srows, srank, sinfo,
-               at<float2>(ws, P.slab_ml_part), at<float2>(ws, P.slab_ml), at<float>(ws, P.cbuf),
-               at<unsigned long long>(ws, P.dgbuf), P.n_chunks, s);
+  CK(launch_slabs(dslabs, (int)P.slabs.size(), P.n_dg_batch, blob_at<int2>(ws, P, P.o_sp),
+                  (int)P.stc_pairs.size() / 2, q, k, S, P.H, P.Hkv, P.D, P.pb.last_q,
+                  tau_of(pb) * 1.4426950408889634f, info, at<int>(ws, P.perm), at<int>(ws, P.rank),
+                  at<uint8_t>(ws, P.labels), srows, srank, sinfo, at<float2>(ws, P.slab_ml_part),
+                  at<float2>(ws, P.slab_ml), at<float>(ws, P.cbuf), at<unsigned long long>(ws, P.dgbuf), P.n_chunks,
+                  s));
   // a3 grid stride / phase
   const DInst* dinsts = blob_at<DInst>(ws, P, P.o_insts);
   launch_grid(dinsts, blob_at<int>(ws, P, P.o_gi), P.n_grid, P.max_ncand, (int)P.insts.size(), dslabs, sinfo, info,
               at<int>(ws, P.perm), at<float>(ws, P.cbuf), at<float>(ws, P.c_rank), S, P.S_pad,
               at<GridRes>(ws, P.gridres), at<double>(ws, P.grid_part), blob_at<int64_t>(ws, P, P.o_gacc),
-              at<unsigned long long>(ws, P.grid_acc), s);
+              at<uint32_t>(ws, P.grid_acc), s);
   // a4 vertical-slash top-k
   launch_vs(dinsts, blob_at<int>(ws, P, P.o_vi), P.n_vs, dslabs, sinfo, info, at<int>(ws, P.perm),
             at<float>(ws, P.cbuf), at<unsigned long long>(ws, P.dgbuf), blob_at<int64_t>(ws, P, P.o_vsl),
@@ -346,6 +341,12 @@ static mmi_status run_sparse(const Plan& P, const mmi_problem* pb, void* ws, con
   A.dbg = g_dbg;
   A.fp_out = fp;
   A.sched = at<unsigned int>(ws, P.sched);
+  // partial rows of work items without a live tile are never written: NaN-fill their LSEs so the
+  // merges of mmi_unpermute skip them (0xFF bytes = NaN)
+  if (P.part_rows > 0) {
+    const cudaError_t ce = cudaMemsetAsync(A.part_lse, 0xFF, sizeof(float) * (size_t)P.part_rows, s);
+    if (ce != cudaSuccess) return fail(MMI_E_CUDA, "partial LSE fill: %s", cudaGetErrorString(ce));
+  }
   AttnLaunch L;
   L.q = q;
   L.qg = at<void>(ws, P.qg);
@@ -402,6 +403,7 @@ extern "C" mmi_status mmi_unpermute(const mmi_problem* pb, const mmi_head_config
   int rows = 0;
   for (int h : P.merge_heads) rows = std::max(rows, P.heads[h].qmod_view >= 0 ? (int)mod_cap : P.nb * BLK);
   launch_merge(C, P.D, blob_at<int>(ws, P, P.o_mh), (int)P.merge_heads.size(), rows, o, lse, s);
+  launch_hrow_merge(C, P.D, blob_at<DHrow>(ws, P, P.o_hr), (int)P.hrows.size(), P.hrow_rows_max, o, lse, s);
   CK(cudaGetLastError());
   return MMI_OK;
 }
@@ -545,7 +547,7 @@ extern "C" mmi_status mmi_export_index(const mmi_problem* pb, const mmi_head_con
   for (const auto& it : items)
     if (it.head == head && it.n_tiles > 0) {
       ++n_it;
-      tiles += (long long)it.n_tiles * (1 + it.has_b);  // computed 128x128 tiles (both halves)
+      tiles += it.pad[1];  // computed 128x128 tiles: live (tile, half) pairs (per-half dead tiles skipped)
       n_seg += it.n_segs;
     }
   out.push_back(n_it);

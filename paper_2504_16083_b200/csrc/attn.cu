@@ -109,7 +109,8 @@ struct Smem {
   // o_empty[2] pv_done[2] sched_full[R] sched_empty[R] kp_full[NKP] kp_empty[NKP]
   static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 14 + 2 * SCHED_RING + 2 * NKP + 4;
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
-  static constexpr int TOTAL = OFF_TMEM + 16;
+  static constexpr int OFF_LIVE = OFF_TMEM + 16;  // [KST] live-half bits of the tile in each K stage
+  static constexpr int TOTAL = OFF_LIVE + 16;
   static constexpr int ALLOC = TOTAL + 1024;  // alignment slack
 };
 
@@ -215,7 +216,11 @@ __device__ __forceinline__ void bit_window(const uint32_t* bits, int lo, uint32_
 
 struct TileInfo {
   int krow;
-  uint32_t space, pred, role, rmode, inst;
+  uint32_t space, role, rmode, inst;
+  uint32_t st0, st1;  // TileState of half A / half B
+  __device__ __forceinline__ uint32_t st(int hf) const { return hf ? st1 : st0; }
+  __device__ __forceinline__ bool pred_any() const { return st0 == TS_PRED || st1 == TS_PRED; }
+  __device__ __forceinline__ uint32_t live() const { return (st0 != TS_DEAD ? 1u : 0u) | (st1 != TS_DEAD ? 2u : 0u); }
 };
 
 // walks the item's segments tile by tile (every warp role keeps its own cursor)
@@ -226,11 +231,19 @@ struct SegIter {
     seg_i = 0;
     t = 0;
     if (P.dense) {
+      // implicit dense causal pair of row blocks (2k, 2k+1): keys 0 .. rb; half A's diagonal is tile
+      // 2k (tile 2k+1 dead for it), half B's diagonal is tile 2k+1
       cur.krow0 = (it.head / (P.H / P.Hkv)) * P.S;
       cur.ntiles = it.rb + 1;
       cur.meta = seg_meta(0, R_TRUE, 0, 0);
-      cur.pred_head = 0;
-      cur.pred_tail = it.has_b ? 2 : 1;  // diagonal tiles of both halves
+      cur.st[0][0] = 0;
+      cur.st[0][1] = 0;
+      cur.st[0][2] = 1;
+      cur.st[0][3] = it.has_b ? 1 : 0;
+      cur.st[1][0] = it.has_b ? 0 : (int16_t)cur.ntiles;
+      cur.st[1][1] = 0;
+      cur.st[1][2] = it.has_b ? 1 : 0;
+      cur.st[1][3] = 0;
     } else {
       cur.ntiles = 0;
       seg_i = -1;
@@ -248,7 +261,8 @@ struct SegIter {
     ti.role = (cur.meta >> 2) & 7u;
     ti.rmode = (cur.meta >> 5) & 1u;
     ti.inst = (cur.meta >> 8) & 0xffu;
-    ti.pred = (t < cur.pred_head || t >= cur.ntiles - cur.pred_tail) ? 1u : 0u;
+    ti.st0 = seg_tile_state(cur, 0, t);
+    ti.st1 = seg_tile_state(cur, 1, t);
     ++t;
     return ti;
   }
@@ -288,6 +302,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int32_t* krank_s = reinterpret_cast<int32_t*>(smem + L::OFF_KRANK);
   volatile int32_t* sched_ring = reinterpret_cast<volatile int32_t*>(smem + L::OFF_SCHED);  // stride SCHED_ENTRY
   int32_t* ri_s = reinterpret_cast<int32_t*>(smem + L::OFF_RI);
+  volatile int32_t* live_s = reinterpret_cast<volatile int32_t*>(smem + L::OFF_LIVE);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -430,15 +445,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int t = 0; t < it.n_tiles; ++t) {
             const TileInfo e = si.next(P, it);
             mbar_wait(empty + stage, phase ^ 1);
+            if (is_k) live_s[stage] = (int)e.live();  // read by the MMA issuer after k_full (release: the arrive below)
             mbar_arrive_expect_tx(full + stage, L::KV_BYTES);
             const CUtensorMap* tm = is_k ? (e.space ? &tmKg : &tmKo) : (e.space ? &tmVg : &tmVo);
             uint8_t* dst = smem + (is_k ? L::OFF_K : L::OFF_V) + stage * L::KV_BYTES;
 #pragma unroll
             for (int c = 0; c < D / 64; ++c) tma_load_2d(dst + c * (BLK * 128), tm, full + stage, c * 64, e.krow);
             // key coordinates of gathered tiles the softmax masks or fingerprints (same predicate there)
-            const bool cp_pos = is_k && (e.pred || P.fingerprint) && e.space;
+            const bool cp_pos = is_k && (e.pred_any() || P.fingerprint) && e.space;
             if (cp_pos) {
-              const bool cp_rank = e.pred && e.rmode;
+              const bool cp_rank = e.pred_any() && e.rmode;
               mbar_wait(kp_empty + kps, kp_phase ^ 1);
               mbar_arrive_expect_tx(kp_full + kps, (cp_rank ? 2 : 1) * BLK * 4);
               bulk_load(kpos_s + kps * BLK, P.kg_pos + e.krow, BLK * 4, kp_full + kps);
@@ -463,6 +479,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // always finds its next scores ready and runs back to back.
       if (elect_one()) {
         constexpr uint32_t IDESC_S = idesc_bf16(128, 64, 0);
+        constexpr uint32_t IDESC_S128 = idesc_bf16(128, 128, 0);
         constexpr uint32_t IDESC_O = idesc_bf16(128, D, 1);
         const uint32_t q_base = smem_u32(smem + L::OFF_Q);
         const uint32_t k_base = smem_u32(smem + L::OFF_K);
@@ -497,9 +514,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               umma_ss(tmem + 128 * hf + 64 * u, ad, bd, IDESC_S, k > 0 ? 1u : 0u);
             }
             umma_commit(s_full + 2 * hf + u);
-            if (j == nsub - 1 && hf == nh - 1) umma_commit(q_empty);  // last S of the item
           };
-          // O_h += P_h(j) V(j), P read from TMEM (A operand), V stage vs
+          // O_h += P_h(j) V(j), P read from TMEM (A operand), V stage vs; `started` bit hf: O_h
+          // already holds a P V of this item
+          uint32_t started = 0;
           auto issue_pv = [&](int hf, int j) {
             const int u = j & 1;
             long long t0 = PROF_T();
@@ -507,28 +525,98 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             PROF_ADD(wp, t0);
             p_bits ^= 1u << (2 * hf + u);
             t0 = PROF_T();
-            if (j == 0) mbar_wait(o_empty + hf, ((o_bits >> hf) & 1u) ^ 1u);  // previous item's epilogue read O_h
+            const bool first = !((started >> hf) & 1u);
+            if (first) mbar_wait(o_empty + hf, ((o_bits >> hf) & 1u) ^ 1u);  // previous item's epilogue read O_h
             PROF_ADD(wo, t0);
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t bd = smem_desc(v_base + vs * L::KV_BYTES + (4 * u + k) * 2048, BLK * 128, 1024, 2);
               umma_ts(tmem + 256 + 128 * hf, tmem + 128 * hf + 64 * u + k * 8, bd, IDESC_O,
-                      (j > 0 || k > 0) ? 1u : 0u);
+                      (!first || k > 0) ? 1u : 0u);
             }
+            started |= 1u << hf;
             umma_commit(pv_done + hf);  // lets the softmax rescale O_h once this P V has landed
-            if (j == nsub - 1) {
-              umma_commit(o_full + hf);
-              o_bits ^= 1u << hf;
-            }
           };
-          // prologue: both sub-tiles of key tile 0 for every half
+          // Tiles dead for a half (no admitted element for its rows, per the index's per-half tile
+          // states) issue neither its S nor its P V; the K loader passes each stage's live-half bits.
+#ifndef MMI_S64
+          // S of a whole 128-key tile is ONE M128 N128 MMA group into both 64-column slots of the
+          // half (full tensor rate: A 4 KB + B 4 KB of shared memory per 64 clk; two N=64 groups
+          // cost 2 x 48 clk, bound by the 128 B/clk operand bandwidth).  S_h(t+1) overwrites P_h(t),
+          // so it is issued right after P_h(t, u=1) V: the other half's work fills the MMA pipe while
+          // this half's softmax runs.
+          auto issue_s128 = [&](int hf, int kst) {
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (k / 4) * (BLK * 128) + (k % 4) * 32;
+              const uint64_t ad = smem_desc(q_base + hf * L::Q_BYTES + off, 16, 1024, 2);
+              const uint64_t bd = smem_desc(k_base + kst * L::KV_BYTES + off, 16, 1024, 2);
+              umma_ss(tmem + 128 * hf, ad, bd, IDESC_S128, k > 0 ? 1u : 0u);
+            }
+            umma_commit(s_full + 2 * hf + 0);
+            umma_commit(s_full + 2 * hf + 1);
+          };
           t0 = PROF_T();
           mbar_wait(k_full + ks, k_phase);
           PROF_ADD(wk, t0);
           tc_fence_after();
+          uint32_t live_cur = (uint32_t)live_s[ks], live_next = 0;
+          for (int hf = 0; hf < nh; ++hf)
+            if ((live_cur >> hf) & 1u) issue_s128(hf, ks);
+          if (n == 1) umma_commit(q_empty);  // last S of the item issued
+          umma_commit(k_empty + ks);
+          if (++ks == KST) {
+            ks = 0;
+            k_phase ^= 1;
+          }
+          for (int t = 0; t < n; ++t) {
+            const bool ahead = (t + 1 < n);
+            t0 = PROF_T();
+            mbar_wait(v_full + vs, v_phase);
+            PROF_ADD(wv, t0);
+            if (ahead) {
+              t0 = PROF_T();
+              mbar_wait(k_full + ks, k_phase);
+              PROF_ADD(wk, t0);
+              tc_fence_after();
+              live_next = (uint32_t)live_s[ks];
+            }
+#ifdef MMI_PROF
+            prof_nt += 2 * nh;
+#endif
+            for (int hf = 0; hf < nh; ++hf)
+              if ((live_cur >> hf) & 1u) issue_pv(hf, 2 * t);
+            for (int hf = 0; hf < nh; ++hf) {
+              if ((live_cur >> hf) & 1u) issue_pv(hf, 2 * t + 1);
+              if (ahead && ((live_next >> hf) & 1u)) issue_s128(hf, ks);
+            }
+            if (t + 1 == n - 1) umma_commit(q_empty);  // last S of the item issued
+            umma_commit(v_empty + vs);
+            if (++vs == VST) {
+              vs = 0;
+              v_phase ^= 1;
+            }
+            if (ahead) {
+              umma_commit(k_empty + ks);
+              if (++ks == KST) {
+                ks = 0;
+                k_phase ^= 1;
+              }
+            }
+            live_cur = live_next;
+          }
+#else
+          // prologue: both sub-tiles of key tile 0 for every live half
+          t0 = PROF_T();
+          mbar_wait(k_full + ks, k_phase);
+          PROF_ADD(wk, t0);
+          tc_fence_after();
+          uint32_t live_cur = (uint32_t)live_s[ks], live_next = 0;
           for (int j = 0; j < 2; ++j)
-            for (int hf = 0; hf < nh; ++hf) issue_s(hf, j, ks);
+            for (int hf = 0; hf < nh; ++hf)
+              if ((live_cur >> hf) & 1u) issue_s(hf, j, ks);
+          if (nsub == 2) umma_commit(q_empty);  // last S of the item issued
           umma_commit(k_empty + ks);
           if (++ks == KST) {
             ks = 0;
@@ -546,15 +634,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_wait(k_full + ks, k_phase);
                 PROF_ADD(wk, t0);
                 tc_fence_after();
+                live_next = (uint32_t)live_s[ks];
               }
             }
 #ifdef MMI_PROF
             prof_nt += nh;
 #endif
             for (int hf = 0; hf < nh; ++hf) {
-              issue_pv(hf, j);
-              if (ahead) issue_s(hf, j + 2, ks);
+              if ((live_cur >> hf) & 1u) issue_pv(hf, j);
+              if (ahead && ((live_next >> hf) & 1u)) issue_s(hf, j + 2, ks);
             }
+            if (j + 2 == nsub - 1) umma_commit(q_empty);  // last S of the item issued
             if (u == 1) {
               umma_commit(v_empty + vs);
               if (++vs == VST) {
@@ -568,8 +658,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                   k_phase ^= 1;
                 }
               }
+              live_cur = live_next;
             }
           }
+#endif
+          // O_h complete for every half that issued a P V (a half with no live tile has no O)
+          for (int hf = 0; hf < nh; ++hf)
+            if ((started >> hf) & 1u) {
+              umma_commit(o_full + hf);
+              o_bits ^= 1u << hf;
+            }
         }
         PROF_ADD(tot, prof_start);
         PROF_FLUSH(0, tot); PROF_FLUSH(1, wp); PROF_FLUSH(2, wk); PROF_FLUSH(3, wv); PROF_FLUSH(4, wq);
@@ -630,7 +728,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         si.init(P, it);
         for (int t = 0; t < it.n_tiles; ++t) {
           const TileInfo e = si.next(P, it);
-          if (e.space && (e.pred || P.fingerprint)) {
+          if (e.space && (e.pred_any() || P.fingerprint)) {
             mbar_wait(kp_full + kps, kp_phase);
             __syncwarp();
             if (lane == 0) mbar_arrive(kp_empty + kps);
@@ -649,7 +747,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       bool write = valid;
       if (it.skip_s > 0 && valid) {
         const int c = it.skip_rank ? xrank : xpos;
-        if (c % it.skip_s == it.skip_p) write = false;
+        if (hline_row(c, it.skip_s, it.skip_p)) write = false;  // owned by the HROW pass
       }
       float m_used = -INFINITY, l_sum = 0.f;
       long long fp_cnt = 0, fp_s1 = 0, fp_s2 = 0;
@@ -660,14 +758,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t* c_sl = nullptr;
       const uint32_t* c_vm = nullptr;
       PROF_ADD(sitem, t0);
+      int n_live = 0;  // tiles of this item live for this half (= P V MMAs into O_h / 2)
+      auto release_kp = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(kp_empty + kps);  // key coordinates of this stage consumed
+        if (++kps == NKP) {
+          kps = 0;
+          kp_phase ^= 1;
+        }
+      };
       for (int t = 0; t < it.n_tiles; ++t) {
         const TileInfo e = si.next(P, it);
-        const uint32_t space = e.space, pred = e.pred, role = e.role, rmode = e.rmode, inst = e.inst;
+        const uint32_t my_st = e.st(hf);
+        // the K loader staged this tile's key coordinates for whichever half masks it
+        const bool kp_stage = e.space && (e.pred_any() || P.fingerprint);
+        if (my_st == TS_DEAD) {  // no admitted element for these rows: no S, no P V for this half
+          if (kp_stage) {
+            mbar_wait(kp_full + kps, kp_phase);
+            release_kp();
+          }
+          continue;
+        }
+        ++n_live;
+        const uint32_t space = e.space, pred = (my_st == TS_PRED) ? 1u : 0u, role = e.role, rmode = e.rmode,
+                       inst = e.inst;
         const bool masked = pred || P.fingerprint;
         uint32_t mw[4] = {0u, 0u, 0u, 0u};  // admitted-key mask of the tile (bit c <-> key c)
         t0 = PROF_T();
+        if (!masked && kp_stage) {  // staged for the other half only
+          mbar_wait(kp_full + kps, kp_phase);
+          release_kp();
+        }
         if (masked) {
-          const bool need_kp = space;
+          const bool need_kp = kp_stage;
           if (need_kp) mbar_wait(kp_full + kps, kp_phase);
           const int* kp = kpos_s + kps * BLK;
           if (valid) {
@@ -691,15 +814,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               // Keys of every view are ascending inside a tile, so each role is at most two
               // index ranges: [0, n_causal) intersected with the pattern's coordinate ranges.
               int n_causal, n_sink, n_lt_local, ybase;
+              const int thr = a_thr(x, local);  // keys y <= thr are outside the local part
               if (!space) {
                 n_causal = min(max(xpos - kbase + 1, 0), BLK);
                 n_sink = min(max(sink - kbase, 0), BLK);
-                n_lt_local = min(max(x - local - kbase + 1, 0), BLK);  // keys with y <= x - local
+                n_lt_local = min(max(thr - kbase + 1, 0), BLK);
                 ybase = kbase;
               } else {
                 const int* yc = rmode ? (krank_s + kps * BLK) : kp;
                 if (role == R_A || role == R_NOTA) {
-                  count_le3(kp, xpos, yc, sink - 1, x - local, n_causal, n_sink, n_lt_local);
+                  count_le3(kp, xpos, yc, sink - 1, thr, n_causal, n_sink, n_lt_local);
                 } else {
                   n_causal = count_le(kp, xpos);
                   n_sink = n_lt_local = 0;
@@ -739,14 +863,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
           }
-          if (need_kp) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(kp_empty + kps);  // key coordinates of this stage consumed
-            if (++kps == NKP) {
-              kps = 0;
-              kp_phase ^= 1;
-            }
-          }
+          if (need_kp) release_kp();
         }
         PROF_ADD(smword, t0);
 #pragma unroll
@@ -861,19 +978,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
       t0 = PROF_T();
-      // ---- epilogue ----
-      mbar_wait(o_full + hf, o_phase);
+      // ---- epilogue ----  (a half with no live tile in this item has no O: it writes zeros / -inf)
+      const bool has_o = n_live > 0;
+      if (has_o) {
+        mbar_wait(o_full + hf, o_phase);
+        o_phase ^= 1;
+        tc_fence_after();
+      }
       PROF_ADD(sepw, t0);
-      o_phase ^= 1;
-      tc_fence_after();
       // no admitted key in this item <=> the running max never left -inf (the polynomial exp2
       // maps masked scores to 2^-125, so l_sum alone does not tell)
       if (m_used == -INFINITY) l_sum = 0.f;
       const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
       const float lse_v = l_sum > 0.f ? (m_used + __log2f(l_sum)) * 0.6931471805599453f : -INFINITY;
       if (P.fingerprint) {
-        tc_fence_before();
-        mbar_arrive(o_empty + hf);
+        if (has_o) {
+          tc_fence_before();
+          mbar_arrive(o_empty + hf);
+        }
         if (write) {
           long long* f = reinterpret_cast<long long*>(P.fp_out) + 3ll * ((long long)it.head * P.S + xpos);
           atomicAdd(reinterpret_cast<unsigned long long*>(f + 0), (unsigned long long)fp_cnt);
@@ -889,9 +1011,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
       for (int c = 0; c < D / 32; c += 2) {  // two 32-column loads in flight per wait
         uint32_t r[2][32];
-        tmem_ld32(tO + c * 32, r[0]);
-        tmem_ld32(tO + c * 32 + 32, r[1]);
-        tmem_wait_ld();
+        if (has_o) {
+          tmem_ld32(tO + c * 32, r[0]);
+          tmem_ld32(tO + c * 32 + 32, r[1]);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[0][j] = r[1][j] = 0u;
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (fin) {
@@ -907,8 +1034,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(o_empty + hf);  // the next item's first P V of this half may start
+      if (has_o) {
+        tc_fence_before();
+        mbar_arrive(o_empty + hf);  // the next item's first P V of this half may start
+      }
       PROF_ADD(sepl, t0);
       // destination row (0: not written).  Partial rows are always written (zeros for invalid rows:
       // the merge weights them by exp(-inf) = 0, which must not meet a NaN).

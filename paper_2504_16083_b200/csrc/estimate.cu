@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(256) slab_kernel(int mode, const DSlab* __rest
   if (threadIdx.x == 0) {
     int ord = 0, n = 0;
     for (int si = 0; si < n_slabs; ++si) {
-      if (slabs[si].kv != kv) continue;
+      if (slabs[si].kv != kv || !slabs[si].need_dg) continue;  // the other slabs run in slab_tc_kernel
       if (ord >= batch * SLAB_BATCH && ord < (batch + 1) * SLAB_BATCH) sm.sl_idx[n++] = si;
       ++ord;
     }
@@ -456,48 +456,59 @@ __global__ void __launch_bounds__(256) slab_kernel(int mode, const DSlab* __rest
   }
 }
 
-__global__ void slab_combine_kernel(const float2* __restrict__ ml_part, int n_chunks, float2* __restrict__ ml) {
+__global__ void slab_combine_kernel(const DSlab* __restrict__ slabs, const float2* __restrict__ ml_part,
+                                    int ml_stride, float2* __restrict__ ml) {
   const int si = blockIdx.x, r = threadIdx.x;
+  const int n_chunks = slabs[si].n_chunks;  // key chunks of the kernel that ran this slab's pass 1
   float m = -INFINITY;
-  for (int c = 0; c < n_chunks; ++c) m = fmaxf(m, ml_part[((size_t)si * n_chunks + c) * SLAB_ROWS + r].x);
+  for (int c = 0; c < n_chunks; ++c) m = fmaxf(m, ml_part[((size_t)si * ml_stride + c) * SLAB_ROWS + r].x);
   float l = 0.f;
   if (m > -INFINITY)
     for (int c = 0; c < n_chunks; ++c) {
-      const float2 p = ml_part[((size_t)si * n_chunks + c) * SLAB_ROWS + r];
+      const float2 p = ml_part[((size_t)si * ml_stride + c) * SLAB_ROWS + r];
       if (p.x > -INFINITY) l += p.y * exp2f(p.x - m);
     }
   ml[si * SLAB_ROWS + r] = make_float2(m, l);
 }
 
+cudaError_t launch_slab_tc(int mode, const int2* pairs, int n_pairs, const DSlab* slabs, const void* q, const void* k,
+                           int S, int Hkv, int D, float scale_log2, const int* rows, const int* sinfo, float2* ml_part,
+                           const float2* ml, float* cbuf, int ml_stride, cudaStream_t st);
+
 template <int D>
-static void launch_slab_passes(dim3 grid, const DSlab* slabs, int n_slabs, const void* q, const void* k, int S, int H,
-                               float scale_log2, int* rows, int* rranks, int* sinfo, const uint8_t* labels,
-                               const int* rank, float2* ml_part, float2* ml, float* cbuf, unsigned long long* dgbuf,
-                               int n_chunks, cudaStream_t st) {
+static cudaError_t launch_slab_dg(int mode, dim3 grid, const DSlab* slabs, int n_slabs, const void* q, const void* k,
+                                  int S, int H, float scale_log2, int* rows, int* rranks, int* sinfo,
+                                  const uint8_t* labels, const int* rank, float2* ml_part, float2* ml, float* cbuf,
+                                  unsigned long long* dgbuf, int n_chunks, cudaStream_t st) {
   const int smem = sizeof(SlabSmem<D>);
-  cudaFuncSetAttribute(slab_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  slab_kernel<D><<<grid, 256, smem, st>>>(0, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S, H,
-                                          scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf, dgbuf,
+  const cudaError_t e = cudaFuncSetAttribute(slab_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  slab_kernel<D><<<grid, 256, smem, st>>>(mode, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S,
+                                          H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf, dgbuf,
                                           n_chunks);
-  slab_combine_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(ml_part, n_chunks, ml);
-  slab_kernel<D><<<grid, 256, smem, st>>>(1, slabs, n_slabs, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, S, H,
-                                          scale_log2, rows, rranks, sinfo, labels, rank, ml_part, ml, cbuf, dgbuf,
-                                          n_chunks);
+  return cudaGetLastError();
 }
 
-void launch_slabs(const DSlab* slabs, int n_slabs, int max_batch, const void* q, const void* k, int S, int H, int Hkv,
-                  int D, int last_q, float scale_log2, const int* info, const int* perm, const int* rank,
-                  const uint8_t* labels, int* rows, int* rranks, int* sinfo, float2* ml_part, float2* ml, float* cbuf,
-                  unsigned long long* dgbuf, int n_chunks, cudaStream_t st) {
-  if (n_slabs == 0) return;
+cudaError_t launch_slabs(const DSlab* slabs, int n_slabs, int n_dg_batch, const int2* stc_pairs, int n_stc_pairs,
+                         const void* q, const void* k, int S, int H, int Hkv, int D, int last_q, float scale_log2,
+                         const int* info, const int* perm, const int* rank, const uint8_t* labels, int* rows,
+                         int* rranks, int* sinfo, float2* ml_part, float2* ml, float* cbuf, unsigned long long* dgbuf,
+                         int ml_stride, cudaStream_t st) {
+  if (n_slabs == 0) return cudaSuccess;
   slab_rows_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(slabs, S, last_q, info, perm, rank, rows, rranks, sinfo);
-  dim3 grid(n_chunks, Hkv, max_batch);
-  if (D == 128)
-    launch_slab_passes<128>(grid, slabs, n_slabs, q, k, S, H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part,
-                            ml, cbuf, dgbuf, n_chunks, st);
-  else
-    launch_slab_passes<64>(grid, slabs, n_slabs, q, k, S, H, scale_log2, rows, rranks, sinfo, labels, rank, ml_part,
-                           ml, cbuf, dgbuf, n_chunks, st);
+  const dim3 grid(ml_stride, Hkv, n_dg_batch);  // slab_kernel: 1024-key chunks (ml_stride of them)
+  cudaError_t e = cudaSuccess;
+  for (int mode = 0; mode < 2 && e == cudaSuccess; ++mode) {
+    if (mode == 1) slab_combine_kernel<<<n_slabs, SLAB_ROWS, 0, st>>>(slabs, ml_part, ml_stride, ml);
+    e = launch_slab_tc(mode, stc_pairs, n_stc_pairs, slabs, q, k, S, Hkv, D, scale_log2, rows, sinfo, ml_part, ml,
+                       cbuf, ml_stride, st);
+    if (e == cudaSuccess && n_dg_batch > 0)
+      e = (D == 128) ? launch_slab_dg<128>(mode, grid, slabs, n_slabs, q, k, S, H, scale_log2, rows, rranks, sinfo,
+                                           labels, rank, ml_part, ml, cbuf, dgbuf, ml_stride, st)
+                     : launch_slab_dg<64>(mode, grid, slabs, n_slabs, q, k, S, H, scale_log2, rows, rranks, sinfo,
+                                          labels, rank, ml_part, ml, cbuf, dgbuf, ml_stride, st);
+  }
+  return e;
 }
 
 // =============================================================== a3: grid
@@ -507,7 +518,7 @@ __global__ void grid_gather_rank_kernel(const DInst* __restrict__ insts, int n_i
                                         const float* __restrict__ cbuf, float* __restrict__ c_rank, int S_pad) {
   const int ii = blockIdx.y;
   const DInst x = insts[ii];
-  if (x.kind != MMI_PAT_GRID || !x.rank) return;
+  if (x.kind != MMI_PAT_GRID || !x.rank || x.stat) return;
   const int na = info[MI_CNT + x.qa];
   const int off = info[MI_OFF + x.qa];
   const DSlab sl = slabs[x.slab];
@@ -537,72 +548,141 @@ __device__ __forceinline__ void grid_window(const DInst& x, const int* sinfo, co
 }
 
 // Fold (reading C4-C6): m_s[p] = sum_{j in W, j = p mod s} c[j] for every candidate stride.
-// One CTA per (group of 32 strides, chunk of W): the chunk of c is converted once
-// to 2^-52 fixed point in shared memory, each stride is reduced thread-per-phase,
-// and the per-chunk sums are flushed with 64-bit integer atomics.  Integer
-// addition is associative, so the fold is exact and order-independent
-// (deterministic) for any schedule.
-// keys per CTA (u64 fixed point in shared memory): one atomic per (stride, phase) and chunk; the
-// fold is issue-bound, so occupancy matters more than the atomic count (12288 measured slower)
+// c >= 0 is a column mass of at most L <= 64 softmax rows, so sum_j c[j] <= 64 and c can be taken
+// to 2^-25 fixed point (round to nearest) with every partial and total sum inside uint32: the
+// fold is exact integer arithmetic, hence order-independent and deterministic.
+// One CTA owns FOLD_SPC consecutive candidate strides and streams the whole window W through
+// shared memory (double-buffered cp.async chunks); thread (group g, phase p) of stride s <= 256
+// sums the chunk elements of absolute phase p at g*s + k*G*s (G = 256 / s groups), threads of
+// larger strides own up to FOLD_MAXW phases each.  Every stride's sums stay in registers across
+// chunks and are written once (no atomics).
 #ifndef MMI_FOLD_CHUNK
-#define MMI_FOLD_CHUNK 4096
+#define MMI_FOLD_CHUNK 8192
 #endif
-constexpr int FOLD_CHUNK = MMI_FOLD_CHUNK;
-constexpr int FOLD_SG = 32;  // strides per CTA
-constexpr double FX52 = 4503599627370496.0;
+constexpr int FOLD_CHUNK = MMI_FOLD_CHUNK;   // u32 keys per shared-memory chunk (32 KB)
+constexpr int FOLD_SPC = 8;                  // candidate strides per CTA
+constexpr int FOLD_THREADS = 256;
+constexpr int FOLD_MAXW = 4;                 // phases per thread for strides in (256, 1024]
+constexpr float FX25 = 33554432.0f;          // 2^25
 
-__global__ void __launch_bounds__(256) grid_acc_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst,
-                                                       const DSlab* __restrict__ slabs, const int* __restrict__ sinfo,
-                                                       const int* __restrict__ info, const float* __restrict__ cbuf,
-                                                       const float* __restrict__ c_rank, int S, int S_pad,
-                                                       const int64_t* __restrict__ acc_off,
-                                                       unsigned long long* __restrict__ acc) {
-  extern __shared__ unsigned long long fold_smem[];
-  unsigned long long* chunk = fold_smem;  // [FOLD_CHUNK] c over this part of W, 2^-52 fixed point
-  __shared__ unsigned long long part[256];
-  const int gi = blockIdx.z;
+__device__ __forceinline__ void fold_load_chunk(uint32_t* dst, const float* __restrict__ c, int j0, int len) {
+  // fixed-point conversion happens at use; raw fp32 bits are staged with cp.async (16 B granules)
+  for (int i = threadIdx.x * 4; i < len; i += FOLD_THREADS * 4) {
+    const int j = j0 + i;
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + i);
+    if (i + 4 <= len && ((j & 3) == 0)) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(c + j) : "memory");
+    } else {
+      for (int e = 0; e < 4 && i + e < len; ++e) dst[i + e] = __float_as_uint(c[j + e]);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(FOLD_THREADS) grid_acc_kernel(const DInst* __restrict__ insts,
+                                                                const int* __restrict__ grid_inst,
+                                                                const DSlab* __restrict__ slabs,
+                                                                const int* __restrict__ sinfo,
+                                                                const int* __restrict__ info,
+                                                                const float* __restrict__ cbuf,
+                                                                const float* __restrict__ c_rank, int S, int S_pad,
+                                                                const int64_t* __restrict__ acc_off,
+                                                                uint32_t* __restrict__ acc) {
+  extern __shared__ __align__(16) uint32_t fold_buf[];  // [2][FOLD_CHUNK]
+  uint32_t(*buf)[FOLD_CHUNK] = reinterpret_cast<uint32_t(*)[FOLD_CHUNK]>(fold_buf);
+  __shared__ uint32_t part[FOLD_THREADS];
+  const int gi = blockIdx.y;
   const DInst x = insts[grid_inst[gi]];
-  const int s0 = x.smin + blockIdx.x * FOLD_SG;
+  if (x.stat) return;  // static grid: nothing to fold
+  const int s0 = x.smin + blockIdx.x * FOLD_SPC;
   if (s0 > x.smax) return;
+  const int ns = min(FOLD_SPC, x.smax - s0 + 1);
   int lo, hi, n;
   grid_window(x, sinfo, info, S, lo, hi, n);
-  const int j_begin = lo + blockIdx.y * FOLD_CHUNK;
-  const int j_end = min(hi, j_begin + FOLD_CHUNK);
-  if (j_begin >= j_end) return;
-  const int len = j_end - j_begin;
-  const int ns = min(FOLD_SG, x.smax - s0 + 1);
   const float* c = x.rank ? c_rank + (size_t)gi * S_pad : cbuf + slabs[x.slab].c_off;
-  for (int i = threadIdx.x; i < len; i += blockDim.x) chunk[i] = (unsigned long long)((double)c[j_begin + i] * FX52);
-  __syncthreads();
-  unsigned long long* g = acc + acc_off[gi];
   const int tid = threadIdx.x;
-  for (int q = 0; q < ns; ++q) {
-    const int s = s0 + q;
-    unsigned long long* gs = g + (size_t)(s - x.smin) * x.smax;
-    const int r = j_begin % s;  // local index i has residue (r + i) mod s
-    if (s <= 256) {
-      const int G = 256 / s;
-      unsigned long long sum = 0;
-      if (tid < G * s) {
-        const int grp = tid / s, p = tid - grp * s;
-        // first local index with (j_begin + i) = p (mod s)
-        const int i0 = p >= r ? p - r : p - r + s;
-        for (int i = i0 + grp * s; i < len; i += G * s) sum += chunk[i];
+  uint32_t accr[FOLD_SPC][FOLD_MAXW];
+#pragma unroll
+  for (int q = 0; q < FOLD_SPC; ++q)
+#pragma unroll
+    for (int w = 0; w < FOLD_MAXW; ++w) accr[q][w] = 0u;
+  const int nchunk = hi > lo ? (hi - lo + FOLD_CHUNK - 1) / FOLD_CHUNK : 0;
+  if (nchunk > 0) fold_load_chunk(buf[0], c, lo, min(FOLD_CHUNK, hi - lo));
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int j_begin = lo + ch * FOLD_CHUNK;
+    const int len = min(FOLD_CHUNK, hi - j_begin);
+    if (ch + 1 < nchunk) {
+      fold_load_chunk(buf[(ch + 1) & 1], c, j_begin + FOLD_CHUNK, min(FOLD_CHUNK, hi - j_begin - FOLD_CHUNK));
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t* cb = buf[ch & 1];
+    // convert this chunk to fixed point in place (each element once)
+    for (int i = tid; i < len; i += FOLD_THREADS) cb[i] = __float2uint_rn(__uint_as_float(cb[i]) * FX25);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < FOLD_SPC; ++q) {
+      const int s = s0 + q;
+      if (q >= ns) break;
+      const int r = j_begin % s;  // local index i has absolute phase (r + i) mod s
+      if (s <= FOLD_THREADS) {
+        const int G = FOLD_THREADS / s;
+        if (tid < G * s) {
+          const int grp = tid / s, p = tid - grp * s;
+          const int i0 = (p >= r ? p - r : p - r + s) + grp * s;
+          const int step = G * s;
+          uint32_t a0 = 0, a1 = 0;
+          int i = i0;
+          for (; i + step < len; i += 2 * step) {
+            a0 += cb[i];
+            a1 += cb[i + step];
+          }
+          if (i < len) a0 += cb[i];
+          accr[q][0] += a0 + a1;
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < FOLD_MAXW; ++w) {
+          const int p = tid + w * FOLD_THREADS;
+          if (p < s) {
+            uint32_t a0 = 0, a1 = 0;
+            int i = p >= r ? p - r : p - r + s;
+            for (; i + s < len; i += 2 * s) {
+              a0 += cb[i];
+              a1 += cb[i + s];
+            }
+            if (i < len) a0 += cb[i];
+            accr[q][w] += a0 + a1;
+          }
+        }
       }
-      part[tid] = sum;
+    }
+    __syncthreads();  // buffer (ch & 1) is refilled two chunks later
+  }
+  // combine the G groups of small strides; write m_s[p]
+  uint32_t* g = acc + acc_off[gi];
+#pragma unroll
+  for (int q = 0; q < FOLD_SPC; ++q) {
+    const int s = s0 + q;
+    if (q >= ns) break;
+    uint32_t* gs = g + (size_t)(s - x.smin) * x.smax;
+    if (s <= FOLD_THREADS) {
+      const int G = FOLD_THREADS / s;
+      part[tid] = (tid < G * s) ? accr[q][0] : 0u;
       __syncthreads();
       if (tid < s) {
-        unsigned long long tot = 0;
+        uint32_t tot = 0;
         for (int grp = 0; grp < G; ++grp) tot += part[grp * s + tid];
-        if (tot) atomicAdd(&gs[tid], tot);
+        gs[tid] = tot;
       }
       __syncthreads();
     } else {
-      for (int p = tid; p < s; p += blockDim.x) {
-        const int i0 = p >= r ? p - r : p - r + s;
-        unsigned long long sum = 0;
-        for (int i = i0; i < len; i += s) sum += chunk[i];
-        if (sum) atomicAdd(&gs[p], sum);
+#pragma unroll
+      for (int w = 0; w < FOLD_MAXW; ++w) {
+        const int p = tid + w * FOLD_THREADS;
+        if (p < s) gs[p] = accr[q][w];
       }
     }
   }
@@ -612,17 +692,17 @@ __global__ void __launch_bounds__(256) grid_acc_kernel(const DInst* __restrict__
 __global__ void __launch_bounds__(256) grid_eval_kernel(const DInst* __restrict__ insts, const int* __restrict__ grid_inst,
                                                         const int* __restrict__ sinfo, const int* __restrict__ info, int S,
                                                         const int64_t* __restrict__ acc_off,
-                                                        const unsigned long long* __restrict__ acc,
+                                                        const uint32_t* __restrict__ acc,
                                                         double* __restrict__ part, GridRes* __restrict__ res) {
   const int gi = blockIdx.y;
   const DInst x = insts[grid_inst[gi]];
   const int s = x.smin + blockIdx.x;
   double* out = part + ((size_t)gi * 1025 + blockIdx.x) * 2;
-  if (s > x.smax) return;
+  if (s > x.smax || x.stat) return;
   int lo, hi, n;
   grid_window(x, sinfo, info, S, lo, hi, n);
   const int N = hi - lo;
-  const unsigned long long* g = acc + acc_off[gi];
+  const uint32_t* g = acc + acc_off[gi];
   // T = sum over all phases of the smallest candidate stride (= sum of c over W, exact)
   typedef cub::BlockReduce<unsigned long long, 256> RU;
   __shared__ typename RU::TempStorage tmpu;
@@ -631,7 +711,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const DInst* __restrict_
   const unsigned long long Tfx = RU(tmpu).Sum(tl);
   __shared__ double T_s;
   if (threadIdx.x == 0) {
-    T_s = (double)Tfx / FX52;
+    T_s = (double)Tfx / (double)FX25;
     if (blockIdx.x == 0) res[gi].T = T_s;
   }
   __syncthreads();
@@ -649,7 +729,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const DInst* __restrict_
   best.J = -INFINITY;
   best.p = INT_MAX;
   for (int p = threadIdx.x; p < s; p += blockDim.x) {
-    const double m = (double)g[(size_t)(s - x.smin) * x.smax + p] / FX52;
+    const double m = (double)g[(size_t)(s - x.smin) * x.smax + p] / (double)FX25;
     const int j0 = lo + (((p - lo) % s) + s) % s;
     const int np = j0 < hi ? (hi - 1 - j0) / s + 1 : 0;
     JP cand;
@@ -680,6 +760,16 @@ __global__ void __launch_bounds__(1024) grid_pick_kernel(const DInst* __restrict
                                                          const double* __restrict__ part, GridRes* __restrict__ res) {
   const int gi = blockIdx.x;
   const DInst x = insts[grid_inst[gi]];
+  if (x.stat) {  // static grid (f3 baselines): fixed stride and phase
+    if (threadIdx.x == 0) {
+      res[gi].s = x.stride;
+      res[gi].p = x.stat_p;
+      res[gi].J = 0.0;
+      res[gi].T = 0.0;
+      res[gi].valid = 1;
+    }
+    return;
+  }
   JS best;
   best.J = -INFINITY;
   best.s = INT_MAX;
@@ -708,16 +798,15 @@ __global__ void __launch_bounds__(1024) grid_pick_kernel(const DInst* __restrict
 void launch_grid(const DInst* insts, const int* grid_inst, int n_grid, int max_ncand, int n_inst_total,
                  const DSlab* slabs, const int* sinfo, const int* info, const int* perm, const float* cbuf,
                  float* c_rank, int S, int S_pad, GridRes* res, double* part, const int64_t* acc_off,
-                 unsigned long long* acc, cudaStream_t st) {
+                 uint32_t* acc, cudaStream_t st) {
   if (n_grid == 0) return;
   grid_gather_rank_kernel<<<dim3(64, n_inst_total), 256, 0, st>>>(insts, n_inst_total, slabs, info, perm, cbuf,
                                                                    c_rank, S_pad);
-  const int n_sg = (max_ncand + FOLD_SG - 1) / FOLD_SG;
-  const int n_ch = (S + FOLD_CHUNK - 1) / FOLD_CHUNK;
-  const int fold_smem = FOLD_CHUNK * (int)sizeof(unsigned long long);
+  const int n_sg = (max_ncand + FOLD_SPC - 1) / FOLD_SPC;
+  const int fold_smem = 2 * FOLD_CHUNK * (int)sizeof(uint32_t);
   cudaFuncSetAttribute(grid_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fold_smem);
-  grid_acc_kernel<<<dim3(n_sg, n_ch, n_grid), 256, fold_smem, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S,
-                                                              S_pad, acc_off, acc);
+  grid_acc_kernel<<<dim3(n_sg, n_grid), FOLD_THREADS, fold_smem, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S,
+                                                                S_pad, acc_off, acc);
   grid_eval_kernel<<<dim3(max_ncand, n_grid), 256, 0, st>>>(insts, grid_inst, sinfo, info, S, acc_off, acc, part, res);
   grid_pick_kernel<<<n_grid, 1024, 0, st>>>(insts, grid_inst, part, res);
 }

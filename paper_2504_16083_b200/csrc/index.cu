@@ -203,23 +203,86 @@ struct RowsInfo {
   int xp_lo, xp_hi;   // positions of first / last valid row
   int xr_lo, xr_hi;   // modality ranks (rank-coordinate views)
 };
+// rows of a work item: the pair (both halves, which fixes the key-tile ranges) and each half
+// (which fixes the per-half tile states)
+struct Rows {
+  RowsInfo R;
+  RowsInfo H[2];
+  int nh;
+};
 
 struct Emitter {
   Seg* out;        // nullptr => count only
-  int n_segs, n_tiles;
-  __device__ __forceinline__ void add(int krow0, int ntiles, uint32_t meta, int ph, int pt) {
+  int n_segs, n_tiles, n_live;  // n_live: live (tile, half) pairs
+  __device__ __forceinline__ void add(int krow0, int ntiles, uint32_t meta, const int (&c)[2][5]) {
     if (ntiles <= 0) return;
     if (out) {
       Seg s;
       s.krow0 = krow0;
       s.ntiles = ntiles;
       s.meta = meta;
-      s.pred_head = (int16_t)min(ph, 32767);
-      s.pred_tail = (int16_t)min(pt, 32767);
+      s.pad = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        s.st[h][0] = (int16_t)c[h][0];
+        s.st[h][1] = (int16_t)c[h][1];
+        s.st[h][2] = (int16_t)c[h][3];
+        s.st[h][3] = (int16_t)c[h][4];
+      }
       out[n_segs] = s;
     }
     ++n_segs;
     n_tiles += ntiles;
+    n_live += 2 * ntiles - c[0][0] - c[0][4] - c[1][0] - c[1][4];
+  }
+};
+
+// Builds segments tile by tile: per half a phase automaton DEAD-head -> PRED-head -> FULL ->
+// PRED-tail -> DEAD-tail (phases 0..4); a tile that would move a half backwards starts a new
+// segment; a tile dead for both halves is dropped.
+struct SegBuilder {
+  int krow_t0, start, n;
+  uint32_t meta;
+  int ph[2];
+  int c[2][5];
+  bool open;
+  __device__ __forceinline__ static int adv(int p, uint32_t st) {
+    if (st == TS_DEAD) return p <= 0 ? 0 : 4;
+    if (st == TS_PRED) return p <= 1 ? 1 : (p <= 3 ? 3 : -1);
+    return p <= 2 ? 2 : -1;
+  }
+  __device__ __forceinline__ void flush(Emitter& E) {
+    if (open && n > 0) E.add(krow_t0 + start * BLK, n, meta, c);
+    open = false;
+  }
+  __device__ __forceinline__ void push(Emitter& E, int t, uint32_t s0, uint32_t s1) {
+    if (s0 == TS_DEAD && s1 == TS_DEAD) {
+      flush(E);
+      return;
+    }
+    int n0 = -1, n1 = -1;
+    if (open && n < SEG_MAX_TILES) {
+      n0 = adv(ph[0], s0);
+      n1 = adv(ph[1], s1);
+    }
+    if (n0 < 0 || n1 < 0) {
+      flush(E);
+      open = true;
+      start = t;
+      n = 0;
+      ph[0] = ph[1] = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) c[h][k] = 0;
+      n0 = adv(0, s0);
+      n1 = adv(0, s1);
+    }
+    ph[0] = n0;
+    ph[1] = n1;
+    c[0][n0]++;
+    c[1][n1]++;
+    ++n;
   }
 };
 
@@ -250,45 +313,39 @@ struct KView {
   }
 };
 
-__device__ __forceinline__ bool tile_full(const KView& kv, int t, uint32_t role, int rmode, const RowsInfo& R,
-                                          int sink, int local) {
+// state of tile t of a K-view for the rows of one half (rows info R; `exists` false for an absent half)
+__device__ __forceinline__ uint32_t tile_state(const KView& kv, int t, uint32_t role, int rmode, const RowsInfo& R,
+                                               bool exists, int sink, int local) {
+  if (!exists) return TS_DEAD;
   const int i0 = t * BLK, i1 = min(t * BLK + BLK - 1, kv.n - 1);
-  if (t * BLK + BLK - 1 >= kv.n) return false;  // pads present
-  const int yp_hi = kv.pos_at(i1);
-  if (yp_hi > R.xp_lo) return false;            // not causally full
-  if (role == R_TRUE) return true;
-  if (role == R_VSSL) return false;
-  const int y_lo = rmode ? (kv.kind == 0 ? i0 : kv.coord_at(i0)) : kv.pos_at(i0);
+  const int yp_lo = kv.pos_at(i0), yp_hi = kv.pos_at(i1);
+  if (yp_lo > R.xp_hi) return TS_DEAD;          // every key after every row of the half
+  const int y_lo = rmode ? (kv.kind == 0 ? i0 : kv.coord_at(i0)) : yp_lo;
   const int y_hi = rmode ? (kv.kind == 0 ? i1 : kv.coord_at(i1)) : yp_hi;
   const int x_lo = rmode ? R.xr_lo : R.xp_lo;
   const int x_hi = rmode ? R.xr_hi : R.xp_hi;
-  if (role == R_A) return (y_hi < sink) || (x_hi - y_lo < local);
-  // R_NOTA
-  return (y_lo >= sink) && (x_lo - y_hi >= local);
+  // the A part of a row x is y < sink or y > thr(x) (thr nondecreasing in x; a_thr, internal.h)
+  if (role == R_A && y_lo >= sink && y_hi <= a_thr(x_lo, local)) return TS_DEAD;   // neither sink nor band
+  if (role == R_NOTA && (y_hi < sink || y_lo > a_thr(x_hi, local))) return TS_DEAD;  // all inside the A part
+  const bool pads = (t * BLK + BLK - 1 >= kv.n);
+  if (pads || yp_hi > R.xp_lo) return TS_PRED;  // pad keys / not causally full
+  if (role == R_TRUE) return TS_FULL;
+  if (role == R_VSSL) return TS_PRED;
+  if (role == R_A) return ((y_hi < sink) || (y_lo > a_thr(x_hi, local))) ? TS_FULL : TS_PRED;
+  return ((y_lo >= sink) && (y_hi <= a_thr(x_lo, local))) ? TS_FULL : TS_PRED;  // R_NOTA
 }
 
-// emit tiles [t0, t1) of a K-view, split into segments of the form PRED* FULL* PRED*
+// emit tiles [t0, t1) of a K-view (segments of per-half DEAD / PRED / FULL runs)
 __device__ void emit_range(Emitter& E, const KView& kv, int t0, int t1, uint32_t role, int rmode, uint32_t inst,
-                           const RowsInfo& R, int sink, int local) {
-  const uint32_t meta = seg_meta(kv.space, role, rmode, inst);
-  int t = t0;
-  while (t < t1) {
-    const int start = t;
-    int ph = 0, nfull = 0, pt = 0;
-    while (t < t1 && !tile_full(kv, t, role, rmode, R, sink, local)) {
-      ++ph;
-      ++t;
-    }
-    while (t < t1 && tile_full(kv, t, role, rmode, R, sink, local)) {
-      ++nfull;
-      ++t;
-    }
-    while (t < t1 && !tile_full(kv, t, role, rmode, R, sink, local)) {
-      ++pt;
-      ++t;
-    }
-    E.add(kv.row0 + start * BLK, t - start, meta, ph, pt);
-  }
+                           const RowsInfo (&RH)[2], int nh, int sink, int local) {
+  SegBuilder b;
+  b.open = false;
+  b.krow_t0 = kv.row0;
+  b.meta = seg_meta(kv.space, role, rmode, inst);
+  for (int t = t0; t < t1; ++t)
+    b.push(E, t, tile_state(kv, t, role, rmode, RH[0], true, sink, local),
+           tile_state(kv, t, role, rmode, RH[1], nh > 1, sink, local));
+  b.flush(E);
 }
 
 // tiles of a K-view whose key coordinate range intersects [c_lo, c_hi] (coords ascending)
@@ -360,7 +417,8 @@ __device__ KView base_kview(const IndexCtx& C, const ItemCtx& I, const DInst& x)
 }
 
 // segments of one pattern instance for MAIN-type rows (and 2D cross pairs of HROW rows)
-__device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& E, const RowsInfo& R) {
+__device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& E, const Rows& RW) {
+  const RowsInfo& R = RW.R;
   const DInst x = C.insts[I.h * MAX_INST + ii];
   if (x.kind == MMI_PAT_NONE) return;
   KView kb = base_kview(C, I, x);
@@ -377,18 +435,18 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
   if (x.kind == MMI_PAT_FULL) {
     int t0, t1;
     range_coords(0, x_hi, t0, t1);
-    emit_range(E, kb, 0, t1, R_TRUE, rmode, ii, R, 0, 0);
+    emit_range(E, kb, 0, t1, R_TRUE, rmode, ii, RW.H, RW.nh, 0, 0);
     return;
   }
   if (x.kind == MMI_PAT_ASHAPE || x.kind == MMI_PAT_GRID) {
     int a0, a1, b0, b1;
     range_coords(0, min(x.sink - 1, x_hi), a0, a1);
-    range_coords(max(0, x_lo - x.local + 1), x_hi, b0, b1);
+    range_coords(max(0, a_thr(x_lo, x.local) + 1), x_hi, b0, b1);
     if (a1 > a0 && b1 > b0 && b0 <= a1) {  // overlapping / adjacent -> one range
-      emit_range(E, kb, min(a0, b0), max(a1, b1), R_A, rmode, ii, R, x.sink, x.local);
+      emit_range(E, kb, min(a0, b0), max(a1, b1), R_A, rmode, ii, RW.H, RW.nh, x.sink, x.local);
     } else {
-      if (a1 > a0) emit_range(E, kb, a0, a1, R_A, rmode, ii, R, x.sink, x.local);
-      if (b1 > b0) emit_range(E, kb, b0, b1, R_A, rmode, ii, R, x.sink, x.local);
+      if (a1 > a0) emit_range(E, kb, a0, a1, R_A, rmode, ii, RW.H, RW.nh, x.sink, x.local);
+      if (b1 > b0) emit_range(E, kb, b0, b1, R_A, rmode, ii, RW.H, RW.nh, x.sink, x.local);
     }
     if (x.kind == MMI_PAT_GRID && (x.flags & GF_V)) {
       const GridRes g = C.gridres[x.grid_id];
@@ -406,7 +464,7 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
       kc.list_rank = 0;
       int t0, t1;
       coord_tiles(kc, 0, x_hi, t0, t1);
-      emit_range(E, kc, 0, t1, R_NOTA, rmode, ii, R, x.sink, x.local);
+      emit_range(E, kc, 0, t1, R_NOTA, rmode, ii, RW.H, RW.nh, x.sink, x.local);
     }
     return;
   }
@@ -426,14 +484,13 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
       // vertical columns: coords of the list (positions, or ranks in rank mode) <= x_hi
       int t0, t1;
       coord_tiles(kc, 0, cross_pos ? R.xp_hi : x_hi, t0, t1);
-      emit_range(E, kc, 0, t1, R_TRUE, rmode, ii, R, 0, 0);
+      emit_range(E, kc, 0, t1, R_TRUE, rmode, ii, RW.H, RW.nh, 0, 0);
     }
     if (!cross_pos) {
       // slash offsets: key coords [x_lo - o, x_hi - o]; ranges move left as o grows
       const int ns = C.vs_cnt[x.vs_id * 2 + 1];
       const int* sl = C.vs_lists + C.vs_list_off[x.vs_id * 2 + 1];
       int cl = 0, ch = -1;
-      const uint32_t meta = seg_meta(kb.space, R_VSSL, rmode, ii);
       for (int q = 0; q < ns; ++q) {
         const int o = sl[q];
         const int c_hi = x_hi - o;
@@ -448,12 +505,12 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
         } else if (t1 - 1 >= cl - 1) {
           cl = min(cl, t0);
         } else {
-          E.add(kb.row0 + cl * BLK, ch - cl + 1, meta, ch - cl + 1, 0);
+          emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0);
           cl = t0;
           ch = t1 - 1;
         }
       }
-      if (ch >= cl) E.add(kb.row0 + cl * BLK, ch - cl + 1, meta, ch - cl + 1, 0);
+      if (ch >= cl) emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0);
     }
     return;
   }
@@ -490,18 +547,21 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
   W.row_mod = -1;
   W.has_b = 0;
   W.pad[0] = W.pad[1] = 0;
-  RowsInfo R;
+  Rows RW;
+  RowsInfo& R = RW.R;
   if (ps.pass == PASS_MAIN) {
     int grp;
     int row_in_view;  // first row of block A in the MAIN view (partial-buffer row)
     if (hd.qmod_view < 0) {
       const int p0 = 2 * b * BLK;
       if (p0 >= C.S) return;
-      R.xp_lo = p0;
-      R.xp_hi = min(C.S, p0 + 2 * BLK) - 1;
-      R.xr_lo = R.xr_hi = 0;
       W.q_row0 = I.h * C.S + p0;
       W.has_b = (p0 + BLK < C.S) ? 1 : 0;
+      for (int hf = 0; hf < 2; ++hf) {
+        RW.H[hf].xp_lo = min(p0 + hf * BLK, C.S - 1);
+        RW.H[hf].xp_hi = min(C.S, p0 + (hf + 1) * BLK) - 1;
+        RW.H[hf].xr_lo = RW.H[hf].xr_hi = 0;
+      }
       row_in_view = p0;
       grp = 0;
     } else {
@@ -519,18 +579,25 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
       }
       if (a < 0) return;
       const int i0 = C.info[MI_PADOFF + a] + 2 * kk * BLK;
-      const int ilast = min(i0 + 2 * BLK - 1, C.info[MI_PADOFF + a] + C.info[MI_CNT + a] - 1);
-      const int p0 = C.modpos[i0];
-      R.xp_lo = p0;
-      R.xp_hi = C.modpos[ilast];
-      R.xr_lo = C.rank[p0];
-      R.xr_hi = C.rank[R.xp_hi];
+      const int iend = C.info[MI_PADOFF + a] + C.info[MI_CNT + a] - 1;  // last valid row of the group
       W.q_row0 = C.views[hd.qmod_view].row_off + i0;
       W.q_gathered = 1;
       W.has_b = (2 * kk + 1 < nblk) ? 1 : 0;
+      for (int hf = 0; hf < 2; ++hf) {
+        const int lo = min(i0 + hf * BLK, iend), hi = min(i0 + (hf + 1) * BLK - 1, iend);
+        RW.H[hf].xp_lo = C.modpos[lo];
+        RW.H[hf].xp_hi = C.modpos[hi];
+        RW.H[hf].xr_lo = C.rank[RW.H[hf].xp_lo];
+        RW.H[hf].xr_hi = C.rank[RW.H[hf].xp_hi];
+      }
       row_in_view = i0;
       grp = a;
     }
+    RW.nh = W.has_b ? 2 : 1;
+    R.xp_lo = RW.H[0].xp_lo;
+    R.xr_lo = RW.H[0].xr_lo;
+    R.xp_hi = RW.H[RW.nh - 1].xp_hi;
+    R.xr_hi = RW.H[RW.nh - 1].xr_hi;
     // skip rows owned by the HROW pass; partial output when the group has a slash pass
     for (int ii = 0; ii < hd.n_inst; ++ii) {
       const DInst x = C.insts[I.h * MAX_INST + ii];
@@ -551,7 +618,7 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
     for (int ii = 0; ii < hd.n_inst; ++ii) {
       const DInst x = C.insts[I.h * MAX_INST + ii];
       if (x.qa >= 0 && x.qa != grp) continue;
-      emit_main(C, I, ii, E, R);
+      emit_main(C, I, ii, E, RW);
     }
   } else {
     const int ii = ps.inst;
@@ -559,13 +626,18 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
     const GridRes g = C.gridres[x.grid_id];
     const int n = x.rank ? C.info[MI_CNT + x.qa] : C.S;
     const int* P_a = x.rank ? C.perm + C.info[MI_OFF + x.qa] : nullptr;
-    int r, t0, nr;
+    int r, t0, nr, chunk = 0;
     if (ps.pass == PASS_HROW) {
+      // split-K (FlashDecoding-style, Alg.5 P:920-947 "sparse load in Q"): slot = (row pair, key chunk)
+      const int n_split = ps.pad0;
+      chunk = b % n_split;
       r = g.p;
       nr = r < n ? (n - r + g.s - 1) / g.s : 0;
-      t0 = 2 * b * BLK;
+      t0 = 2 * (b / n_split) * BLK;
       const DView qv = C.views[x.v_cls_q];
       W.q_row0 = qv.row_off + t0;
+      W.out_mode = OUT_PARTIAL;
+      W.out_row0 = x.pad[1] + chunk * qv.cap + t0;
     } else {
       // pair b inside residue class r: classes r < rem hold q+1 keys, the others q
       ClassGeo cg;
@@ -592,33 +664,43 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
     }
     if (t0 >= nr) return;
     W.has_b = (t0 + BLK < nr) ? 1 : 0;
-    const int tl = min(t0 + 2 * BLK - 1, nr - 1);
-    const int c_lo = r + g.s * t0, c_hi = r + g.s * tl;
+    RW.nh = W.has_b ? 2 : 1;
     W.q_gathered = 1;
     W.row_mod = ps.qa;
-    if (x.rank) {
-      R.xr_lo = c_lo;
-      R.xr_hi = c_hi;
-      R.xp_lo = P_a[c_lo];
-      R.xp_hi = P_a[c_hi];
-    } else {
-      R.xp_lo = c_lo;
-      R.xp_hi = c_hi;
-      R.xr_lo = R.xr_hi = 0;
+    for (int hf = 0; hf < 2; ++hf) {
+      const int ta = min(t0 + hf * BLK, nr - 1), tb = min(t0 + (hf + 1) * BLK - 1, nr - 1);
+      const int ca = r + g.s * ta, cb = r + g.s * tb;
+      if (x.rank) {
+        RW.H[hf].xr_lo = ca;
+        RW.H[hf].xr_hi = cb;
+        RW.H[hf].xp_lo = P_a[ca];
+        RW.H[hf].xp_hi = P_a[cb];
+      } else {
+        RW.H[hf].xp_lo = ca;
+        RW.H[hf].xp_hi = cb;
+        RW.H[hf].xr_lo = RW.H[hf].xr_hi = 0;
+      }
     }
+    R.xp_lo = RW.H[0].xp_lo;
+    R.xr_lo = RW.H[0].xr_lo;
+    R.xp_hi = RW.H[RW.nh - 1].xp_hi;
+    R.xr_hi = RW.H[RW.nh - 1].xr_hi;
+    const int c_hi = x.rank ? R.xr_hi : R.xp_hi;
     W.pad[0] = R.xp_lo;
     if (ps.pass == PASS_HROW) {
-      // the whole causal row of the pattern's key base (role TRUE)
+      // the whole causal row of the pattern's key base (role TRUE), key chunk `chunk`
       DInst xf = x;
       xf.kind = MMI_PAT_FULL;
       KView kb = base_kview(C, I, xf);
       int tt0, tt1;
-      coord_tiles(kb, 0, x.rank ? R.xr_hi : R.xp_hi, tt0, tt1);
-      emit_range(E, kb, 0, tt1, R_TRUE, x.rank, ii, R, 0, 0);
-      if (hd.boundary == MMI_BND_2D) {
+      coord_tiles(kb, 0, c_hi, tt0, tt1);
+      const int k0 = chunk * HROW_SPLIT_TILES, k1 = min(tt1, k0 + HROW_SPLIT_TILES);
+      if (k0 >= k1) return;   // the rows of this pair are shorter than the chunk start
+      emit_range(E, kb, k0, k1, R_TRUE, x.rank, ii, RW.H, RW.nh, 0, 0);
+      if (hd.boundary == MMI_BND_2D && chunk == 0) {
         for (int jj = 0; jj < hd.n_inst; ++jj) {
           const DInst y = C.insts[I.h * MAX_INST + jj];
-          if (y.qa == x.qa && y.kb != x.qa) emit_main(C, I, jj, E, R);
+          if (y.qa == x.qa && y.kb != x.qa) emit_main(C, I, jj, E, RW);
         }
       }
     } else {
@@ -638,7 +720,7 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
       kc.list_rank = 0;
       int tt0, tt1;
       coord_tiles(kc, 0, c_hi, tt0, tt1);
-      emit_range(E, kc, 0, tt1, R_NOTA, x.rank, ii, R, x.sink, x.local);
+      emit_range(E, kc, 0, tt1, R_NOTA, x.rank, ii, RW.H, RW.nh, x.sink, x.local);
     }
   }
 }
@@ -648,7 +730,7 @@ __global__ void items_count_kernel(IndexCtx C) {
   if (slot >= C.n_slots) return;
   Emitter E;
   E.out = nullptr;
-  E.n_segs = E.n_tiles = 0;
+  E.n_segs = E.n_tiles = E.n_live = 0;
   WorkItem W;
   build_slot(C, slot, E, W);
   C.seg_cnt[slot] = E.n_segs;
@@ -659,7 +741,7 @@ __global__ void items_fill_kernel(IndexCtx C) {
   if (slot >= C.n_slots) return;
   Emitter E;
   const int off = C.seg_off[slot];
-  E.n_segs = E.n_tiles = 0;
+  E.n_segs = E.n_tiles = E.n_live = 0;
   WorkItem W;
   if ((int64_t)off + C.seg_cnt[slot] > C.seg_cap) {
     // the plan's segment bound was short: never write past the region; the item stays empty
@@ -669,6 +751,7 @@ __global__ void items_fill_kernel(IndexCtx C) {
     build_slot(C, slot, E, W);
     W.seg_off = off;
     W.n_segs = W.n_tiles = 0;
+    W.pad[1] = 0;
     C.items[slot] = W;
     C.sort_keys[slot] = ~0;
     C.sort_vals[slot] = slot;
@@ -679,13 +762,14 @@ __global__ void items_fill_kernel(IndexCtx C) {
   W.seg_off = off;
   W.n_segs = E.n_segs;
   W.n_tiles = E.n_tiles;
+  W.pad[1] = E.n_live;
   C.items[slot] = W;
   // work order: long items first by length (LPT); short items by position then head,
   // so that concurrently running CTAs share the key tiles of a KV group in L2.
   // (sorted ascending on the bitwise complement: descending key, equal keys keep slot order)
   int key = 0;
-  if (E.n_tiles >= LONG_ITEM_TILES)
-    key = 0x40000000 + E.n_tiles;
+  if (E.n_live >= 2 * LONG_ITEM_TILES)
+    key = 0x40000000 + E.n_live;
   else if (E.n_tiles > 0)
     key = 0x3FFFFFFF - ((W.pad[0] / BLK) * 64 + (W.head & 63));
   C.sort_keys[slot] = ~key;
@@ -758,17 +842,27 @@ __global__ void merge_kernel(IndexCtx C, const int* __restrict__ heads_list, int
       const GridRes g = C.gridres[x.grid_id];
       const int coord = x.rank ? C.rank[pos] : pos;
       const int r = coord % g.s;
-      if ((x.flags & GF_H) && r == g.p) {
+      if ((x.flags & GF_H) && hline_row(coord, g.s, g.p)) {
         pos = -1;  // written by the HROW pass
       } else {
+        // a partial row whose work item had no live tile was never written: its LSE is the NaN
+        // fill of mmi_sparse_prefill and it contributes nothing (its O row is not read)
         j0 = hd.part_rows0 + i;
-        const float l0 = C.part_lse[j0];
+        float l0 = C.part_lse[j0];
+        if (!(l0 > -INFINITY)) {
+          l0 = -INFINITY;
+          j0 = -1;
+        }
         float l1 = -INFINITY;
         if (!(r == g.p && (x.flags & (GF_H | GF_V)))) {
           ClassGeo cg;
           cg.init(x.rank ? C.info[MI_CNT + x.qa] : C.S, g.s);
           j1 = x.pad[0] + cg.classoff(r) + coord / g.s;
           l1 = C.part_lse[j1];
+          if (!(l1 > -INFINITY)) {
+            l1 = -INFINITY;
+            j1 = -1;
+          }
         }
         const float m = fmaxf(l0, l1);
         w0 = (l0 == -INFINITY) ? 0.f : __expf(l0 - m);
@@ -792,7 +886,7 @@ __global__ void merge_kernel(IndexCtx C, const int* __restrict__ heads_list, int
       a[r] = VH{};
       b[r] = VH{};
       if (p >= 0) {
-        a[r] = *reinterpret_cast<const VH*>(C.part_o + q0 * D + CPL * lane);
+        if (q0 >= 0) a[r] = *reinterpret_cast<const VH*>(C.part_o + q0 * D + CPL * lane);
         if (q1 >= 0) b[r] = *reinterpret_cast<const VH*>(C.part_o + q1 * D + CPL * lane);
       }
     }
@@ -817,7 +911,70 @@ __global__ void merge_kernel(IndexCtx C, const int* __restrict__ heads_list, int
   if (lane < MERGE_R && pos >= 0 && lse) lse[(size_t)h * C.S + pos] = lsev;
 }
 
+// ================================================================ split-K merge of h-line rows (a8)
+// One warp per h-line row: the row's key chunks c = 0 .. x_tile / HROW_SPLIT_TILES (every chunk that
+// holds one of its causal keys; later chunks hold none) are LSE-merged (Alg.5 P:940-942 rescaling,
+// generalised to n partials) in fp32 and written to token order.
+template <int CPL>
+__global__ void hrow_merge_kernel(IndexCtx C, const DHrow* __restrict__ hrows, int max_rows,
+                                  __nv_bfloat16* __restrict__ o, float* __restrict__ lse) {
+  constexpr int D = 32 * CPL;
+  const DHrow hr = hrows[blockIdx.y];
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const DInst x = C.insts[hr.head * MAX_INST + hr.inst];
+  const DView qv = C.views[x.v_cls_q];
+  if (i >= max_rows || i >= qv.cap) return;
+  const int pos = C.qg_pos[qv.row_off + i];
+  if (pos < 0 || pos >= C.S) return;
+  if (hr.qa >= 0 && C.labels[pos] != hr.qa) return;   // Q-boundary: a row of another modality
+  const GridRes g = C.gridres[x.grid_id];
+  const int coord = g.p + g.s * i;                      // key-base coordinate (position or rank)
+  const int nc = min(coord / BLK / HROW_SPLIT_TILES + 1, hr.n_split);
+  const long long base = x.pad[1] + i;
+  float m = -INFINITY;
+  for (int c = lane; c < nc; c += 32) {
+    const float l = C.part_lse[base + (long long)c * qv.cap];
+    if (l > -INFINITY) m = fmaxf(m, l);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  float acc[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) acc[k] = 0.f;
+  float wsum = 0.f;
+  for (int c = 0; c < nc; ++c) {
+    const long long row = base + (long long)c * qv.cap;
+    const float l = C.part_lse[row];
+    if (!(l > -INFINITY)) continue;  // empty chunk for this row (or never written: NaN fill)
+    const float w = __expf(l - m);
+    wsum += w;
+    const __half* src = C.part_o + row * D + CPL * lane;
+#pragma unroll
+    for (int k = 0; k < CPL; k += 2) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(src + k));
+      acc[k] += w * f.x;
+      acc[k + 1] += w * f.y;
+    }
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  __nv_bfloat16* dst = o + ((size_t)hr.head * C.S + pos) * D + CPL * lane;
+#pragma unroll
+  for (int k = 0; k < CPL; k += 2)
+    *reinterpret_cast<__nv_bfloat162*>(dst + k) = __floats2bfloat162_rn(acc[k] * inv, acc[k + 1] * inv);
+  if (lse && lane == 0) lse[(size_t)hr.head * C.S + pos] = wsum > 0.f ? m + __logf(wsum) : -INFINITY;
+}
+
 // ================================================================ launchers
+void launch_hrow_merge(const IndexCtx& C, int D, const DHrow* hrows, int n_hrows, int max_rows, void* o, float* lse,
+                       cudaStream_t st) {
+  if (n_hrows <= 0 || max_rows <= 0) return;
+  const dim3 grid((unsigned)((max_rows * 32 + 255) / 256), n_hrows);
+  if (D == 128)
+    hrow_merge_kernel<4><<<grid, 256, 0, st>>>(C, hrows, max_rows, (__nv_bfloat16*)o, lse);
+  else
+    hrow_merge_kernel<2><<<grid, 256, 0, st>>>(C, hrows, max_rows, (__nv_bfloat16*)o, lse);
+}
 void launch_build_views(const IndexCtx& C, const int* qviews, int nq, const int* kviews, int nk, int64_t qrows,
                         int64_t krows, cudaStream_t st) {
   if (qrows > 0) build_views_kernel<<<(unsigned)((qrows + 255) / 256), 256, 0, st>>>(C, 0, qviews, nq, qrows);

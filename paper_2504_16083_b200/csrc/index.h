@@ -49,6 +49,8 @@ void launch_items_fill(const IndexCtx& C, cudaStream_t st);
 void launch_items_gather(const IndexCtx& C, cudaStream_t st);
 void launch_gather(const int* src, int64_t rows, int D, const void* a, void* a_out, const void* b, void* b_out,
                    cudaStream_t st);
+void launch_hrow_merge(const IndexCtx& C, int D, const DHrow* hrows, int n_hrows, int max_rows, void* o, float* lse,
+                       cudaStream_t st);
 void launch_merge(const IndexCtx& C, int D, const int* heads_list, int n_heads, int n_rows, void* o, float* lse,
                   cudaStream_t st);
 

@@ -18,18 +18,42 @@ constexpr unsigned FLAG_SEG_OVERFLOW = 2u;  // the index needed more tile segmen
 // meta bits: [0] space (0 = original K/V, 1 = gathered K̄/V̄), [2,5) role,
 // [5] coordinate system of the pattern (0 = original position, 1 = modality
 // rank), [8,16) instance id (index into the head's InstParam table).
-// Tiles t < pred_head and t >= ntiles - pred_tail evaluate the element
-// predicate (PRED); the others are admitted entirely (FULL).
+// Every tile has a state per query half (the two 128-row blocks of a work
+// item): DEAD (no admitted element for any row of the half: no MMA, no
+// softmax), PRED (the element predicate is evaluated) or FULL (every element
+// admitted).  Per half the segment's tiles read
+//     DEAD^dh  PRED^ph  FULL*  PRED^pt  DEAD^dt      (st[half] = {dh, ph, pt, dt})
+// and a tile is in the segment only if it is live for at least one half.
 enum Role : uint32_t { R_TRUE = 0, R_A = 1, R_NOTA = 2, R_VSSL = 3 };
+enum TileState : uint32_t { TS_DEAD = 0, TS_PRED = 1, TS_FULL = 2 };
+constexpr int SEG_MAX_TILES = 32767;   // per-half counts are int16
 struct Seg {
   int32_t krow0;      // K-space row of the first key of the first tile
   int32_t ntiles;
   uint32_t meta;
-  int16_t pred_head, pred_tail;
+  int32_t pad;
+  int16_t st[2][4];   // per half: dead head, pred head, pred tail, dead tail
 };
+static_assert(sizeof(Seg) == 32, "Seg is two 16-byte loads");
 __host__ __device__ inline uint32_t seg_meta(uint32_t space, uint32_t role, uint32_t rank, uint32_t inst) {
   return space | (role << 2) | (rank << 5) | (inst << 8);
 }
+__host__ __device__ inline uint32_t seg_tile_state(const Seg& s, int half, int t) {
+  const int dh = s.st[half][0], ph = s.st[half][1], pt = s.st[half][2], dt = s.st[half][3];
+  if (t < dh || t >= s.ntiles - dt) return TS_DEAD;
+  if (t < dh + ph || t >= s.ntiles - dt - pt) return TS_PRED;
+  return TS_FULL;
+}
+
+// Last key coordinate NOT in the local part of the A part of query coordinate x: the local band
+// is y > x - local (local >= 1), or, in block mode (local < 0, SparseTransformer fixed, reading
+// C23), the query's segment y >= floor(x / L) * L of L = -local keys.  Nondecreasing in x.
+__host__ __device__ inline int a_thr(int x, int local) {
+  return local >= 0 ? x - local : x - x % (-local) - 1;
+}
+// h-line rows of a grid with stride s and phase p: x = p (mod s) and x >= p (a static grid uses
+// s = 1, p = S - bottom for the tri-shape's dense bottom rows)
+__host__ __device__ inline bool hline_row(int x, int s, int p) { return x >= p && (x - p) % s == 0; }
 
 // ---- pattern instance parameters for the kernel (after estimation) ----
 struct InstParam {
@@ -57,7 +81,7 @@ struct WorkItem {
   int32_t skip_rank;  //     coord system of the skip test
   int32_t row_mod;    // >=0: only rows of this modality are valid (Q-boundary class views)
   int32_t has_b;      // 1: the item also covers the next 128-row block (rows q_row0 + 128 ...)
-  int32_t pad[2];
+  int32_t pad[2];     // [0] first row position (work-order key), [1] live (tile, half) pairs
 };
 
 struct AttnParams {

@@ -6,6 +6,7 @@
 
 #include "plan.h"
 #include "sort.h"
+#include "estimate.h"
 
 namespace mmi {
 
@@ -41,9 +42,48 @@ static mmi_status check_pattern(const mmi_pattern& p, bool cross, int h, const c
       if (p.stride == 0 && (p.stride_min < 1 || p.stride_max < p.stride_min || p.stride_max > 1024))
         return bad(MMI_E_CONFIG, "searched grid needs 1 <= stride_min <= stride_max <= 1024");
       return MMI_OK;
+    case MMI_PAT_TRISHAPE:
+      if (cross) return bad(MMI_E_CONFIG, "tri-shape on a cross-modality pair");
+      if (p.local < 1 || p.sink < 0 || p.bottom < 0) return bad(MMI_E_CONFIG, "tri-shape needs local >= 1, sink >= 0, bottom >= 0");
+      return MMI_OK;
+    case MMI_PAT_SF_FIXED:
+    case MMI_PAT_SF_STRIDED:
+      if (cross) return bad(MMI_E_CONFIG, "SparseTransformer pattern on a cross-modality pair");
+      if (p.local < 1) return bad(MMI_E_CONFIG, "SparseTransformer pattern needs local >= 1");
+      if (p.stride < 1 || p.stride > 1024) return bad(MMI_E_UNSUPPORTED, "SparseTransformer stride not in [1, 1024]");
+      return MMI_OK;
     default:
       return bad(MMI_E_INVALID, "unknown pattern kind");
   }
+}
+
+// the static baselines execute as grids with a fixed (stride, phase) and no estimation:
+//   TRISHAPE(sink, local, bottom) -> h-lines on the rows x >= S - bottom (stride 1, phase S - bottom)
+//   SF_FIXED(l, stride)           -> v-lines y = 0 (mod stride), A part = the query's l-key segment
+//   SF_STRIDED(l, stride)         -> slash lines (x - y) = 0 (mod stride), A part = local window l
+static mmi_pattern as_grid(const mmi_pattern& p, int S, int& stat, int& stat_p) {
+  stat = 0;
+  stat_p = 0;
+  if (p.kind < MMI_PAT_TRISHAPE) return p;
+  mmi_pattern g = p;
+  g.kind = MMI_PAT_GRID;
+  g.use_hline = g.use_vline = g.use_slash = 0;
+  stat = 1;
+  if (p.kind == MMI_PAT_TRISHAPE) {
+    g.stride = 1;
+    g.use_hline = 1;
+    stat_p = std::max(0, S - p.bottom);
+  } else {
+    g.sink = 0;
+    if (p.kind == MMI_PAT_SF_FIXED) {
+      g.use_vline = 1;
+      g.local = -p.local;  // block mode
+    } else {
+      g.use_slash = 1;
+    }
+  }
+  g.stride_min = g.stride_max = g.stride;
+  return g;
 }
 
 mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P, std::string& err) {
@@ -75,6 +115,15 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
         return MMI_E_CONFIG;
       }
       if ((st = check_pattern(c.intra[0], false, h, "intra[0]", err)) != MMI_OK) return st;
+    } else if (c.boundary == MMI_BND_Q || c.boundary == MMI_BND_2D) {
+      for (int a = 0; a < M; ++a)
+        for (int b = 0; b < M; ++b)
+          if ((c.boundary == MMI_BND_Q ? (b == 0 ? c.intra[a].kind : 0) : c.pair[a][b].kind) == MMI_PAT_TRISHAPE) {
+            err = "head " + std::to_string(h) + ": tri-shape is supported on No/K-boundary heads only";
+            return MMI_E_CONFIG;
+          }
+    }
+    if (c.boundary == MMI_BND_NONE || c.boundary == MMI_BND_K) {
     } else if (c.boundary == MMI_BND_Q) {
       for (int m = 0; m < M; ++m) {
         if (c.intra[m].kind == MMI_PAT_NONE) {
@@ -141,8 +190,12 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
     if (c.boundary == MMI_BND_2D) hd.kmod_view = add_view(VK_MOD, 1, mod_cap, h, -1, -1, 0);
     int slab_of_group[MAX_MOD] = {-1, -1, -1, -1};
     int n = 0;
-    auto add_inst = [&](const mmi_pattern& p, int qa, int kb, int rank) {
+    auto add_inst = [&](const mmi_pattern& p_in, int qa, int kb, int rank) {
+      int stat = 0, stat_p = 0;
+      const mmi_pattern p = as_grid(p_in, S, stat, stat_p);
       DInst& x = P.insts[(size_t)h * MAX_INST + n];
+      x.stat = stat;
+      x.stat_p = stat_p;
       x.kind = p.kind;
       x.rank = rank;
       x.qa = qa;
@@ -157,7 +210,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
       x.flags = (p.use_hline ? GF_H : 0) | (p.use_vline ? GF_V : 0) | (p.use_slash ? GF_SL : 0);
       x.force = (kb < 0 || qa == kb) ? 1 : 0;
       const int grp = qa < 0 ? 0 : qa;
-      if (needs_est(p)) {
+      if (needs_est(p) && !stat) {
         if (slab_of_group[grp] < 0) {
           DSlab sl;
           memset(&sl, 0, sizeof(sl));
@@ -176,7 +229,11 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
       if (p.kind == MMI_PAT_GRID) {
         x.grid_id = P.n_grid++;
         const int vk = rank ? VK_RANK_CLASS : VK_ORIG_CLASS;
-        const int64_t cls_cap = pad128((nbase + x.smin - 1) / x.smin) + BLK;
+        // class-p views: every (S - p) / s rows; a static grid knows its phase (tri-shape: the
+        // bottom rows only)
+        const int64_t cls_n = stat ? std::max<int64_t>(0, (nbase - stat_p + x.smin - 1) / x.smin)
+                                   : (nbase + x.smin - 1) / x.smin;
+        const int64_t cls_cap = pad128(cls_n) + BLK;
         const int64_t res_cap = pad128(nbase + (int64_t)x.smax * BLK) + BLK;
         if (p.use_hline) x.v_cls_q = add_view(vk, 0, cls_cap, h, n, rank ? qa : -1, 1);
         if (p.use_slash) x.v_res_q = add_view(vk, 0, res_cap, h, n, rank ? qa : -1, 0);
@@ -217,6 +274,36 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
     P.slabs[i].c_off = (int64_t)i * P.S_pad;
     P.slabs[i].dg_off = (int64_t)i * P.S_pad;
   }
+  // slab kernels: slabs whose diagonal mass is needed run in slab_kernel (batches of 4 per KV
+  // group); the others are packed two per tcgen05 M=128 tile (same KV group)
+  {
+    std::vector<int> dg_per_kv(P.Hkv, 0);
+    for (int kv = 0; kv < P.Hkv; ++kv) {
+      int pending = -1;
+      for (size_t i = 0; i < P.slabs.size(); ++i) {
+        if (P.slabs[i].kv != kv) continue;
+        if (P.slabs[i].need_dg) {
+          dg_per_kv[kv]++;
+          continue;
+        }
+        if (pending < 0) {
+          pending = (int)i;
+        } else {
+          P.stc_pairs.push_back(pending);
+          P.stc_pairs.push_back((int)i);
+          pending = -1;
+        }
+      }
+      if (pending >= 0) {
+        P.stc_pairs.push_back(pending);
+        P.stc_pairs.push_back(-1);
+      }
+    }
+    for (int c : dg_per_kv) P.n_dg_batch = std::max(P.n_dg_batch, (c + 3) / 4);
+    const int n_old = (S + SLAB_CHUNK - 1) / SLAB_CHUNK;
+    const int n_tc = slab_tc_chunks(S);
+    for (auto& sl : P.slabs) sl.n_chunks = sl.need_dg ? n_old : n_tc;
+  }
   P.qg_rows = qrow + BLK;
   P.kg_rows = krow + BLK;
 
@@ -232,6 +319,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
   };
   int slot = 0;
   int64_t segcap = 0;
+  int64_t part_rows_hrow_cursor = P.part_rows;  // HROW split-K partial rows follow the MAIN / SLASH ones
   for (int h = 0; h < H; ++h) {
     const DHead& hd = P.heads[h];
     const bool modq = hd.qmod_view >= 0;
@@ -256,7 +344,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
       }
       per_main = std::max(per_main, s);
     }
-    segcap += per_main * mp.n_slots;
+    segcap += (3 * per_main + 2) * mp.n_slots;
     for (int i = 0; i < hd.n_inst; ++i) {
       const DInst& x = P.insts[(size_t)h * MAX_INST + i];
       if (x.kind != MMI_PAT_GRID) continue;
@@ -267,17 +355,32 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
           if (y.qa == x.qa && y.kb != x.qa) cross += segbound(y);
         }
       if (x.v_cls_q >= 0) {
+        // split-K: (row pair, key chunk of HROW_SPLIT_TILES tiles of the key base)
+        const int64_t base_keys = (hd.boundary == MMI_BND_2D) ? S : (int64_t)S;  // upper bound of n_a too
+        const int n_split = (int)std::max<int64_t>(1, (base_keys + (int64_t)HROW_SPLIT_TILES * BLK - 1) /
+                                                           ((int64_t)HROW_SPLIT_TILES * BLK));
+        const int n_pairs = (P.views[x.v_cls_q].cap / BLK + 1) / 2 + 1;
         DPass p2;
         memset(&p2, 0, sizeof(p2));
         p2.head = h;
         p2.pass = PASS_HROW;
         p2.inst = i;
         p2.qa = (hd.boundary == MMI_BND_Q) ? x.qa : -1;
-        p2.n_slots = (P.views[x.v_cls_q].cap / BLK + 1) / 2 + 1;
+        p2.pad0 = n_split;
+        p2.n_slots = n_pairs * n_split;
         p2.slot_base = slot;
         slot += p2.n_slots;
         P.passes.push_back(p2);
-        segcap += (1 + cross) * p2.n_slots;
+        segcap += (3 + 3 * cross) * p2.n_slots;
+        P.insts[(size_t)h * MAX_INST + i].pad[1] = (int32_t)part_rows_hrow_cursor;
+        part_rows_hrow_cursor += (int64_t)n_split * P.views[x.v_cls_q].cap;
+        DHrow hr;
+        hr.head = h;
+        hr.inst = i;
+        hr.qa = p2.qa;
+        hr.n_split = n_split;
+        P.hrows.push_back(hr);
+        P.hrow_rows_max = std::max(P.hrow_rows_max, P.views[x.v_cls_q].cap);
       }
       if (x.v_res_q >= 0) {
         DPass p3;
@@ -290,12 +393,13 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
         p3.slot_base = slot;
         slot += p3.n_slots;
         P.passes.push_back(p3);
-        segcap += 1 * p3.n_slots;
+        segcap += 3 * p3.n_slots;
       }
     }
   }
   P.n_slots = slot;
   P.seg_cap = segcap + 16;
+  P.part_rows = part_rows_hrow_cursor;
 
   // VS lists / bitmaps
   const int64_t bitw = (int64_t)S / 32 + 8;  // slack: 128-bit windows may read past S
@@ -364,6 +468,8 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
     for (int h = 0; h < H; ++h)
       if (P.heads[h].part_rows0 >= 0) P.merge_heads.push_back(h);
     sub(P.o_mh, sizeof(int) * std::max<size_t>(P.merge_heads.size(), 1));
+    sub(P.o_hr, sizeof(DHrow) * std::max<size_t>(P.hrows.size(), 1));
+    sub(P.o_sp, sizeof(int) * std::max<size_t>(P.stc_pairs.size(), 2));
     P.blob_bytes = b;
   }
   reg(P.blob, P.blob_bytes);
@@ -442,6 +548,8 @@ std::vector<uint8_t> make_blob(const Plan& P) {
   put(P.o_vsb, P.vs_off_tab.data() + 2 * nv, sizeof(int64_t) * 2 * nv);
   put(P.o_gacc, P.gacc_off.data(), sizeof(int64_t) * P.gacc_off.size());
   put(P.o_mh, P.merge_heads.data(), sizeof(int) * P.merge_heads.size());
+  put(P.o_hr, P.hrows.data(), sizeof(DHrow) * P.hrows.size());
+  put(P.o_sp, P.stc_pairs.data(), sizeof(int) * P.stc_pairs.size());
   return b;
 }
 

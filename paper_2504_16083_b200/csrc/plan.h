@@ -18,6 +18,10 @@ constexpr int FOLD_LO = 128;     // reading C6
 constexpr int FOLD_GAP = 128;    // reading C6
 constexpr int SLAB_ROWS = 64;    // max last_q
 constexpr int SLAB_CHUNK = 1024; // keys per slab CTA (8 tiles)
+#ifndef MMI_HROW_SPLIT
+#define MMI_HROW_SPLIT 128
+#endif
+constexpr int HROW_SPLIT_TILES = MMI_HROW_SPLIT;  // split-K chunk of an h-line row pair (16384 keys)
 
 enum PassKind : int32_t { PASS_MAIN = 0, PASS_HROW = 1, PASS_SLASH = 2 };
 enum ViewKind : int32_t { VK_ORIG_CLASS = 0, VK_RANK_CLASS = 1, VK_MOD = 2, VK_VCOL = 3 };
@@ -32,7 +36,10 @@ struct DInst {
   int32_t grid_id, vs_id;              // result slots (-1)
   int32_t v_cls_q, v_res_q, v_cls_k, v_res_k, v_vcol;  // view ids (-1)
   int32_t force;                       // VS: force column 0 / offset 0
-  int32_t pad[2];
+  int32_t pad[2];                      // [0] slash partial-row base, [1] HROW split-K partial-row base
+  // static grid (the f3 baselines): fixed (stride, stat_p), no estimation; local < 0
+  // means "block mode": the A part is the query's segment of -local keys (SF fixed)
+  int32_t stat, stat_p, pad2[2];
 };
 struct DView {
   int32_t kind;       // ViewKind
@@ -45,13 +52,18 @@ struct DView {
 };
 struct DSlab {
   int32_t head, kv, qmod, rank_mode;   // qmod: modality of the slab rows (-1: last rows overall)
-  int32_t need_dg, pad0, pad1, pad2;   // need_dg: a vertical-slash instance with slashes uses this slab
+  int32_t need_dg, n_chunks, pad1, pad2; // need_dg: a vertical-slash instance with slashes uses this slab
+                                       // (slab_kernel); else the tcgen05 slab kernel; n_chunks: key chunks of
+                                       // its pass-1 statistics
   int64_t c_off;                       // float offset of c[S]
   int64_t dg_off;                      // u64 offset of dg[S]
 };
 struct DPass {
   int32_t head, pass, inst, n_slots;   // inst: grid instance (HROW/SLASH), -1 for MAIN
-  int32_t slot_base, qa, pad0, pad1;   // qa: Q-bnd HROW/SLASH modality filter (-1 none)
+  int32_t slot_base, qa, pad0, pad1;   // qa: Q-bnd HROW/SLASH modality filter (-1 none); pad0: HROW key chunks
+};
+struct DHrow {                         // one h-line (HROW) pass: its split-K partials are merged by hrow_merge
+  int32_t head, inst, qa, n_split;
 };
 struct DHead {
   int32_t boundary, n_inst, inst_base, kv;
@@ -99,6 +111,12 @@ struct Plan {
   size_t o_gacc = 0;
   std::vector<int> merge_heads;        // heads with partial rows (LSE merge in mmi_unpermute)
   size_t o_mh = 0;
+  std::vector<DHrow> hrows;            // HROW passes (split-K merge in mmi_unpermute)
+  std::vector<int> stc_pairs;          // tcgen05 slab kernel: (slab a, slab b or -1) per packed M=128 tile
+  size_t o_sp = 0;
+  int n_dg_batch = 0;                  // slab_kernel batches (slabs with need_dg, per KV group / 4)
+  size_t o_hr = 0;
+  int hrow_rows_max = 0;
   // workspace regions
   Region blob;
   Region labels, mod_cnt, mod_off, perm, rank, modpos, modrank;

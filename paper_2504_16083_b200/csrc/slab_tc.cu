@@ -1,0 +1,256 @@
+// Last-q slab estimation on the 5th-generation tensor cores:
+//   A-hat = softmax(Q[R] K^T tau + m_causal)   (Alg.1; P:241 per-modality slabs)
+//   c[j]  = sum_r A-hat[r, j]                    (column mass: grid fold / verticals)
+// Two passes over the keys of one KV group: pass 1 = per-row running max / sum (online
+// softmax statistics, partial per key chunk, combined by slab_combine_kernel), pass 2 =
+// A-hat tile by tile and its column sums.  The slabs of one KV group are packed two per
+// tcgen05 M=128 tile (rows 0-63 slab a, 64-127 slab b); S = Q K^T (M128 N128) goes to a
+// double-buffered TMEM accumulator, K tiles arrive by TMA (128B swizzle) in a 2-stage ring,
+// and 4 epilogue warps (thread = TMEM lane = slab row) run the exp2 / statistics.  Column
+// sums over a warp's 32 rows use a butterfly transpose-reduce (31 shuffles per 32 columns),
+// the two warps of a slab are added in shared memory: fixed order, deterministic.
+// Slabs that also need the diagonal mass dg (vertical-slash heads with slashes) run in
+// slab_kernel (estimate.cu), which accumulates both.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "estimate.h"
+#include "ptx.cuh"
+
+namespace mmi {
+
+constexpr int STC_THREADS = 256;   // warp 0 TMA, warp 1 MMA + TMEM, warps 2-3 Q staging, warps 4-7 epilogue
+constexpr int STC_KST = 2;         // K ring stages
+constexpr int STC_CHUNK_TILES = 64;  // key tiles per CTA (8192 keys)
+
+template <int D>
+struct StcSmem {
+  static constexpr int Q_BYTES = BLK * D * 2;
+  static constexpr int K_BYTES = BLK * D * 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_CS = OFF_K + STC_KST * K_BYTES;       // [4 warps][128] column partials
+  static constexpr int OFF_BAR = OFF_CS + 4 * BLK * 4;
+  static constexpr int N_BAR = 2 * STC_KST + 4;                  // k_full, k_empty, s_full[2], s_empty[2]
+  static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
+  static constexpr int TOTAL = OFF_TMEM + 16;
+  static constexpr int ALLOC = TOTAL + 1024;
+};
+
+// butterfly transpose-reduce: v[k] = this lane's value of column k (32 columns); returns the sum
+// over the 32 lanes of column `lane`
+__device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const float send = upper ? v[k] : v[k + o];
+      const float keep = upper ? v[k + o] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0];
+}
+
+template <int D>
+__global__ void __launch_bounds__(STC_THREADS, 2)
+    slab_tc_kernel(const __grid_constant__ CUtensorMap tmK, int mode, const int2* __restrict__ pairs,
+                   const DSlab* __restrict__ slabs, const __nv_bfloat16* __restrict__ q, int S, float scale_log2,
+                   const int* __restrict__ rows, const int* __restrict__ sinfo, float2* __restrict__ ml_part,
+                   const float2* __restrict__ ml, float* __restrict__ cbuf, int ml_stride) {
+  using L = StcSmem<D>;
+  extern __shared__ __align__(1024) uint8_t stc_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(stc_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* k_full = bars;
+  uint64_t* k_empty = bars + STC_KST;
+  uint64_t* s_full = bars + 2 * STC_KST;
+  uint64_t* s_empty = s_full + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+  float* cs = reinterpret_cast<float*>(smem + L::OFF_CS);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int chunk = blockIdx.x;
+  const int2 pr = pairs[blockIdx.y];
+  const int sa = pr.x, sb = pr.y;  // slab b may be -1
+  const DSlab SA = slabs[sa];
+  const int kv = SA.kv;
+  int maxpos = sinfo[sa * 4 + 2];
+  if (sb >= 0) maxpos = max(maxpos, sinfo[sb * 4 + 2]);
+  const int t_begin = chunk * STC_CHUNK_TILES;
+  const int t_end = min(t_begin + STC_CHUNK_TILES, maxpos / BLK + 1);
+  const int nt = t_end - t_begin;
+  // row identity of epilogue thread (TMEM lane = row of the packed tile)
+  const int r = (warp >= 4) ? (warp - 4) * 32 + lane : 0;
+  const int my_slab = (r < 64) ? sa : sb;
+  const int rl = r & 63;
+  const int my_pos = (warp >= 4 && my_slab >= 0) ? rows[my_slab * SLAB_ROWS + rl] : -1;
+  if (nt <= 0) {  // every key of this chunk is after every slab row
+    if (mode == 0 && warp >= 4 && my_slab >= 0)
+      ml_part[((size_t)my_slab * ml_stride + chunk) * SLAB_ROWS + rl] = make_float2(-INFINITY, 0.f);
+    return;
+  }
+  // ---- Q tile (two slabs, 128 rows) -> shared memory in the UMMA 128B-swizzle K-major layout ----
+  {
+    constexpr int CPR = D / 8;  // 16-byte chunks per row
+    for (int idx = threadIdx.x; idx < BLK * CPR; idx += STC_THREADS) {
+      const int row = idx / CPR, ck = idx % CPR;
+      const int sl = (row < 64) ? sa : sb;
+      int pos = -1;
+      if (sl >= 0) pos = rows[sl * SLAB_ROWS + (row & 63)];
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (pos >= 0) val = __ldg(reinterpret_cast<const uint4*>(q + ((size_t)slabs[sl].head * S + pos) * D) + ck);
+      const int cb = ck / 8, k = ck % 8;  // 64-column block, 16-byte unit inside the 128-byte row
+      *reinterpret_cast<uint4*>(smem + L::OFF_Q + cb * (BLK * 128) + row * 128 + ((k ^ (row & 7)) * 16)) = val;
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STC_KST; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(s_empty + i, 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_holder);
+  fence_proxy_async_smem();  // generic-proxy Q stores visible to the tensor core
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmK);
+      for (int i = 0; i < nt; ++i) {
+        const int st = i % STC_KST;
+        mbar_wait(k_empty + st, ((i / STC_KST) & 1) ^ 1);
+        mbar_arrive_expect_tx(k_full + st, L::K_BYTES);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_2d(smem + L::OFF_K + st * L::K_BYTES + c * (BLK * 128), &tmK, k_full + st, c * 64,
+                      kv * S + (t_begin + i) * BLK);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t IDESC = idesc_bf16(128, 128, 0);
+      const uint32_t q_base = smem_u32(smem + L::OFF_Q), k_base = smem_u32(smem + L::OFF_K);
+      for (int i = 0; i < nt; ++i) {
+        const int st = i % STC_KST, b = i & 1;
+        mbar_wait(k_full + st, (i / STC_KST) & 1);
+        mbar_wait(s_empty + b, ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * (BLK * 128) + (k % 4) * 32;
+          umma_ss(tmem + b * 128, smem_desc(q_base + off, 16, 1024, 2),
+                  smem_desc(k_base + st * L::K_BYTES + off, 16, 1024, 2), IDESC, k > 0 ? 1u : 0u);
+        }
+        umma_commit(k_empty + st);
+        umma_commit(s_full + b);
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    const bool valid = my_pos >= 0;
+    float m = -INFINITY, l = 0.f, inv_l = 0.f;
+    if (mode == 1 && valid) {
+      const float2 v = ml[(size_t)my_slab * SLAB_ROWS + rl];
+      m = v.x;
+      inv_l = v.y > 0.f ? 1.f / v.y : 0.f;
+    }
+    for (int i = 0; i < nt; ++i) {
+      const int b = i & 1;
+      const int j0 = (t_begin + i) * BLK;
+      mbar_wait(s_full + b, (i >> 1) & 1);
+      tc_fence_after();
+      // keys j0 + c admitted for this row iff j0 + c <= pos (causal; pos < S)
+      const int n_ok = valid ? min(max(my_pos - j0 + 1, 0), BLK) : 0;
+#pragma unroll
+      for (int c = 0; c < BLK / 32; ++c) {
+        uint32_t raw[32];
+        tmem_ld32(tmem + b * 128 + c * 32 + lane_off, raw);
+        tmem_wait_ld();
+        float v[32];
+        if (mode == 0) {
+          float mx = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            v[k] = (c * 32 + k < n_ok) ? __uint_as_float(raw[k]) * scale_log2 : -INFINITY;
+            mx = fmaxf(mx, v[k]);
+          }
+          const float mn = fmaxf(m, mx);
+          if (mn > -INFINITY) {
+            float sum = 0.f;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) sum += ex2(v[k] - mn);
+            l = (m > -INFINITY ? l * ex2(m - mn) : 0.f) + sum;
+            m = mn;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            v[k] = (c * 32 + k < n_ok) ? ex2(__uint_as_float(raw[k]) * scale_log2 - m) * inv_l : 0.f;
+          const float colsum = warp_colsum32(v, lane);  // column c*32 + lane over this warp's 32 rows
+          cs[ew * BLK + c * 32 + lane] = colsum;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty + b);  // S buffer b may be overwritten
+      if (mode == 1) {
+        named_bar_sync(1, 128);
+        // thread t (0..127) owns key column t: slab a = warps 0+1, slab b = warps 2+3
+        const int t = ew * 32 + lane, j = j0 + t;
+        if (j < S) {
+          cbuf[SA.c_off + j] = cs[t] + cs[BLK + t];
+          if (sb >= 0) cbuf[slabs[sb].c_off + j] = cs[2 * BLK + t] + cs[3 * BLK + t];
+        }
+        named_bar_sync(1, 128);
+      }
+    }
+    if (mode == 0 && my_slab >= 0)
+      ml_part[((size_t)my_slab * ml_stride + chunk) * SLAB_ROWS + rl] = make_float2(m, l);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+int make_tmap_rows(CUtensorMap* m, const void* base, long long rows, int D);
+
+int slab_tc_chunks(int S) { return (S + STC_CHUNK_TILES * BLK - 1) / (STC_CHUNK_TILES * BLK); }
+
+cudaError_t launch_slab_tc(int mode, const int2* pairs, int n_pairs, const DSlab* slabs, const void* q, const void* k,
+                           int S, int Hkv, int D, float scale_log2, const int* rows, const int* sinfo, float2* ml_part,
+                           const float2* ml, float* cbuf, int ml_stride, cudaStream_t st) {
+  if (n_pairs <= 0) return cudaSuccess;
+  CUtensorMap tm;
+  if (make_tmap_rows(&tm, k, (long long)Hkv * S, D) != 0) return cudaErrorInvalidValue;
+  const dim3 grid(slab_tc_chunks(S), n_pairs);
+  cudaError_t e;
+  if (D == 128) {
+    e = cudaFuncSetAttribute(slab_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, StcSmem<128>::ALLOC);
+    if (e != cudaSuccess) return e;
+    slab_tc_kernel<128><<<grid, STC_THREADS, StcSmem<128>::ALLOC, st>>>(
+        tm, mode, pairs, slabs, (const __nv_bfloat16*)q, S, scale_log2, rows, sinfo, ml_part, ml, cbuf, ml_stride);
+  } else {
+    e = cudaFuncSetAttribute(slab_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, StcSmem<64>::ALLOC);
+    if (e != cudaSuccess) return e;
+    slab_tc_kernel<64><<<grid, STC_THREADS, StcSmem<64>::ALLOC, st>>>(
+        tm, mode, pairs, slabs, (const __nv_bfloat16*)q, S, scale_log2, rows, sinfo, ml_part, ml, cbuf, ml_stride);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace mmi

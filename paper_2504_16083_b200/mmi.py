@@ -34,7 +34,7 @@ class c_pattern(ctypes.Structure):
                 ("n_vertical", ctypes.c_int32), ("n_slash", ctypes.c_int32), ("stride", ctypes.c_int32),
                 ("stride_min", ctypes.c_int32), ("stride_max", ctypes.c_int32),
                 ("use_hline", ctypes.c_uint8), ("use_vline", ctypes.c_uint8), ("use_slash", ctypes.c_uint8),
-                ("_pad", ctypes.c_uint8)]
+                ("_pad", ctypes.c_uint8), ("bottom", ctypes.c_int32)]
 
 
 class c_head_config(ctypes.Structure):
@@ -88,7 +88,7 @@ def _check(st: int):
 
 def to_c_pattern(p: Pattern) -> c_pattern:
     return c_pattern(p.kind, p.sink, p.local, p.n_vertical, p.n_slash, p.stride, p.stride_min, p.stride_max,
-                     int(p.use_hline), int(p.use_vline), int(p.use_slash), 0)
+                     int(p.use_hline), int(p.use_vline), int(p.use_slash), 0, p.bottom)
 
 
 def to_c_configs(cfgs: Sequence[HeadConfig]):

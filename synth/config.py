@@ -17,11 +17,14 @@ from dataclasses import dataclass, field
 from typing import List, Optional
 
 KIND_NONE, KIND_FULL, KIND_ASHAPE, KIND_VSLASH, KIND_GRID = 0, 1, 2, 3, 4
+# static baseline patterns of the paper's evaluation (tab:impl_details P:685-688)
+KIND_TRISHAPE, KIND_SF_FIXED, KIND_SF_STRIDED = 5, 6, 7
 BND_NONE, BND_K, BND_Q, BND_2D = 0, 1, 2, 3
 MAX_MOD = 4
 
 KIND_NAMES = {KIND_NONE: "none", KIND_FULL: "full", KIND_ASHAPE: "ashape",
-              KIND_VSLASH: "vslash", KIND_GRID: "grid"}
+              KIND_VSLASH: "vslash", KIND_GRID: "grid", KIND_TRISHAPE: "trishape",
+              KIND_SF_FIXED: "sf_fixed", KIND_SF_STRIDED: "sf_strided"}
 BND_NAMES = {BND_NONE: "none", BND_K: "k", BND_Q: "q", BND_2D: "2d"}
 
 
@@ -38,11 +41,16 @@ class Pattern:
     use_hline: bool = False
     use_vline: bool = False
     use_slash: bool = False
+    bottom: int = 0          # Tri-shape: the last `bottom` query rows attend to every key
 
     def describe(self) -> str:
         k = KIND_NAMES[self.kind]
         if self.kind == KIND_ASHAPE:
             return f"ashape({self.sink},{self.local})"
+        if self.kind == KIND_TRISHAPE:
+            return f"trishape({self.sink},{self.local},{self.bottom})"
+        if self.kind in (KIND_SF_FIXED, KIND_SF_STRIDED):
+            return f"{k}({self.local},{self.stride})"
         if self.kind == KIND_VSLASH:
             return f"vs({self.n_vertical},{self.n_slash})"
         if self.kind == KIND_GRID:
@@ -64,6 +72,25 @@ def grid(stride: int = 0, h: bool = True, v: bool = True, sl: bool = False,
          sink: int = 128, local: int = 128, stride_min: int = 2, stride_max: int = 1024) -> Pattern:
     return Pattern(kind=KIND_GRID, stride=stride, stride_min=stride_min, stride_max=stride_max,
                    use_hline=h, use_vline=v, use_slash=sl, sink=sink, local=local)
+
+
+def trishape(sink: int = 128, local: int = 4096, bottom: int = 128) -> Pattern:
+    """Tri-shape (tab:impl_details P:688): A-shape plus dense rows for the last `bottom`
+    queries ("full attention for all tokens to the last window's queries")."""
+    return Pattern(kind=KIND_TRISHAPE, sink=sink, local=local, bottom=bottom)
+
+
+def sf_fixed(local: int = 256, stride: int = 256) -> Pattern:
+    """SparseTransformer fixed (tab:impl_details P:686, Local = vline_stride = tokens per
+    frame): attention inside the query's segment of `local` tokens plus every segment's initial
+    token (keys y = 0 mod stride) -- reading C23."""
+    return Pattern(kind=KIND_SF_FIXED, local=local, stride=stride)
+
+
+def sf_strided(local: int = 256, stride: int = 256) -> Pattern:
+    """SparseTransformer strided (tab:impl_details P:687): a local window of `local`
+    tokens plus dilated lines x - y = 0 mod stride -- reading C23."""
+    return Pattern(kind=KIND_SF_STRIDED, local=local, stride=stride)
 
 
 def full() -> Pattern:

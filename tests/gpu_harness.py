@@ -10,6 +10,7 @@ import numpy as np
 import torch
 
 from synth.config import (KIND_NONE, KIND_FULL, KIND_ASHAPE, KIND_VSLASH, KIND_GRID,
+                          KIND_TRISHAPE, KIND_SF_FIXED, KIND_SF_STRIDED,
                           BND_NONE, BND_K, BND_Q, BND_2D, MAX_MOD)
 from oracle.estimate import estimate_head
 from oracle.pipeline import run_head
@@ -59,7 +60,7 @@ def _patterns(cfg, M) -> List:
     return [cfg.pair[a][b] for a in range(M) for b in range(M) if cfg.pair[a][b].kind != KIND_NONE]
 
 
-def gpu_index_as_oracle(cfg, exp: Dict, M: int) -> Dict:
+def gpu_index_as_oracle(cfg, exp: Dict, M: int, S: int = 0) -> Dict:
     """Rebuild an oracle-style index dict from the GPU's exported index."""
     pats = _patterns(cfg, M)
     inst = []
@@ -71,6 +72,10 @@ def gpu_index_as_oracle(cfg, exp: Dict, M: int) -> Dict:
             inst.append(dict(kind=KIND_VSLASH, V=e["V"], Sl=e["Sl"]))
         elif p.kind == KIND_ASHAPE:
             inst.append(dict(kind=KIND_ASHAPE, sink=p.sink, local=p.local))
+        elif p.kind == KIND_TRISHAPE:
+            inst.append(dict(kind=p.kind, sink=p.sink, local=p.local, bottom=p.bottom, n=S))
+        elif p.kind in (KIND_SF_FIXED, KIND_SF_STRIDED):
+            inst.append(dict(kind=p.kind, local=p.local, stride=p.stride))
         else:
             inst.append(dict(kind=p.kind))
     if cfg.boundary in (BND_NONE, BND_K):
@@ -153,7 +158,7 @@ def check_head(wl, d, gpu, h: int, rows: Optional[np.ndarray] = None, check_inde
     if same_index:
         r = r_own
     else:
-        gidx = gpu_index_as_oracle(cfg, gpu["exp"][h], pb.n_modalities)
+        gidx = gpu_index_as_oracle(cfg, gpu["exp"][h], pb.n_modalities, pb.seq_len)
         r = run_head(pb, cfg, qh, kg, vg, d["labels"], rows=rows, index=gidx)
     rr = r["rows"]
     ridx = torch.from_numpy(rr).to(gpu["o"].device)

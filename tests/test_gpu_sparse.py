@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 import torch
 
-from synth.config import HeadConfig, Problem, grid, ashape, vslash, full, none
+from synth.config import HeadConfig, Problem, grid, ashape, vslash, full, none, trishape, sf_fixed, sf_strided
 from synth.workloads import build_workload, small_workload, _qwen_heads, GRID_FLAGS
 from synth.gen import gen_qkv
 from gpu_harness import run_gpu, check_head, assert_head
@@ -165,3 +165,19 @@ def test_label_out_of_range_flag():
     assert sp.flags() & 1
     sp(q, k, v, lab)
     assert sp.flags() == 0
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_static_baseline_patterns(D):
+    """f3: Tri-shape, SparseTransformer fixed / strided (tab:impl_details
+    P:685-688) as static grids on the same kernel: exact fingerprints, O / LSE within tolerance."""
+    heads = [HeadConfig.no_boundary(trishape(128, 512, 128)), HeadConfig.no_boundary(trishape(16, 64, 300)),
+             HeadConfig.no_boundary(sf_fixed(256, 256)), HeadConfig.no_boundary(sf_fixed(100, 37)),
+             HeadConfig.no_boundary(sf_strided(256, 256)), HeadConfig.no_boundary(sf_strided(50, 3)),
+             HeadConfig.q_boundary([sf_fixed(256, 256), sf_strided(64, 5)]),
+             HeadConfig.two_d([[sf_strided(128, 7), none()], [ashape(64, 200), sf_fixed(64, 16)]])]
+    wl = small_workload(S_frames=3, interleave=4, text_len=200, H=len(heads), Hkv=2, D=D, heads=heads)
+    d = gen_qkv(wl, seed=21)
+    g = run_gpu(wl, d)
+    for h in range(len(heads)):
+        _assert_head(check_head(wl, d, g, h))

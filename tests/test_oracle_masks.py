@@ -12,7 +12,9 @@ from oracle.modality import modality_groups, inverse_permutation, residue_permut
 from oracle.attention import fingerprint, masked_attention, dense_causal_attention
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "mask_fixtures.json")))
-KINDS = {"none": KIND_NONE, "full": KIND_FULL, "ashape": KIND_ASHAPE, "vslash": KIND_VSLASH, "grid": KIND_GRID}
+from synth.config import KIND_TRISHAPE, KIND_SF_FIXED, KIND_SF_STRIDED
+KINDS = {"none": KIND_NONE, "full": KIND_FULL, "ashape": KIND_ASHAPE, "vslash": KIND_VSLASH, "grid": KIND_GRID,
+         "trishape": KIND_TRISHAPE, "sf_fixed": KIND_SF_FIXED, "sf_strided": KIND_SF_STRIDED}
 
 
 def _inst(d):
@@ -167,3 +169,38 @@ def test_residue_causality_rule():
             for j in range(40):
                 rq, tq, rk, tk = i % s, i // s, j % s, j // s
                 assert (j <= i) == (tk <= tq - (1 if rk > rq else 0))
+
+
+def test_static_baseline_patterns_lines_and_special_cases():
+    """f3 patterns: vectorised masks == an explicit union of their line / block sets,
+    and the degenerate parameters reduce to full causal attention."""
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        S = int(rng.integers(3, 50))
+        lab = np.zeros(S, dtype=np.uint8)
+        _, rho, _ = modality_groups(lab, 1)
+        l, st, sink, b = int(rng.integers(1, 9)), int(rng.integers(1, 9)), int(rng.integers(0, 4)), int(rng.integers(0, 6))
+        want = {k: np.zeros((S, S), dtype=bool) for k in ("tri", "fix", "str")}
+        for i in range(S):
+            for j in range(i + 1):
+                want["tri"][i, j] = j < sink or i - j < l or i >= S - b
+        for i in range(S):                       # segments of l keys + every segment's initial key
+            want["fix"][i, (i // l) * l:i + 1] = True
+            want["fix"][i, 0:i + 1:st] = True
+        for i in range(S):                       # local window + dilated diagonals
+            want["str"][i, max(0, i - l + 1):i + 1] = True
+            for o in range(0, i + 1, st):
+                want["str"][i, i - o] = True
+        insts = {"tri": dict(kind=KIND_TRISHAPE, sink=sink, local=l, bottom=b, n=S),
+                 "fix": dict(kind=KIND_SF_FIXED, local=l, stride=st),
+                 "str": dict(kind=KIND_SF_STRIDED, local=l, stride=st)}
+        for k, inst in insts.items():
+            M = head_mask_rows(BND_NONE, dict(intra=[inst]), lab, rho, np.arange(S), S)
+            assert (M == want[k]).all(), (k, S, l, st)
+    S = 20
+    lab = np.zeros(S, dtype=np.uint8)
+    _, rho, _ = modality_groups(lab, 1)
+    for inst in [dict(kind=KIND_TRISHAPE, sink=0, local=1, bottom=S, n=S), dict(kind=KIND_SF_FIXED, local=S, stride=7),
+                 dict(kind=KIND_SF_STRIDED, local=1, stride=1), dict(kind=KIND_SF_FIXED, local=1, stride=1)]:
+        M = head_mask_rows(BND_NONE, dict(intra=[inst]), lab, rho, np.arange(S), S)
+        assert (M == _causal(S)).all(), inst
