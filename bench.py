@@ -69,13 +69,15 @@ def _patterns(cfg, M=2):
     return [(p, m) for p, m in out if p.kind != KIND_NONE]
 
 
-def count_launches(heads) -> int:
+def count_launches(heads, fused: int = 1) -> int:
     """Kernels of libmmi.so launched per step (every one is this library's own kernel)."""
+    from synth.config import KIND_TRISHAPE, KIND_SF_FIXED, KIND_SF_STRIDED
     pats = [p for c in heads for p, _ in _patterns(c)]
+    static = [p for p in pats if p.kind in (KIND_TRISHAPE, KIND_SF_FIXED, KIND_SF_STRIDED)]
     n = 4                                   # modality count / scan / place / pad
     if any(p.kind in (KIND_GRID, KIND_VSLASH) for p in pats):
         n += 4                              # slab rows, pass 1, combine, pass 2
-    if any(p.kind == KIND_GRID for p in pats):
+    if any(p.kind == KIND_GRID for p in pats) or static:
         n += 4                              # gather-rank, fold, eval, pick
     if any(p.kind == KIND_VSLASH for p in pats):
         n += 1                              # vs select
@@ -84,9 +86,10 @@ def count_launches(heads) -> int:
     n += 1                                  # items fill
     n += 8                                  # LPT sort: 4 radix passes x (histogram, scatter)
     n += 1                                  # items gather
-    n += 2                                  # permute gathers
+    n += 0 if fused == 3 else (1 if fused == 1 else 2)  # permute gathers (K/V; Q fused into the attention loads)
     n += 1                                  # sparse attention
-    n += int(any(p.kind == KIND_GRID and p.use_slash for p in pats))  # LSE merge
+    n += int(any((p.kind == KIND_GRID and p.use_slash) or p.kind == KIND_SF_STRIDED for p in pats))  # LSE merge
+    n += int(any((p.kind == KIND_GRID and p.use_hline) or p.kind == KIND_TRISHAPE for p in pats))   # h-row merge
     return n
 
 
@@ -439,16 +442,19 @@ def main():
     st = mmi.mmi_plan_stats(lpb, lheads)
     hbm_peak = float(peaks["hbm_gbs"])
     alg = {
-        # gathered Q-bar / K-bar / V-bar rows: read + write, bf16
-        "permute": ((moved["qg_read"] + moved["qg_written"] + 2 * (moved["kg_read"] + moved["kg_written"])) * D * 2,
-                    "(rows read + rows written) of Qbar, Kbar, Vbar x D x 2 B (mmi_traffic_stats)"),
+        # gathered Q-bar / K-bar / V-bar rows: read + write, bf16 (0: permutation fused into the attention loads)
+        "permute": (((0 if st["fused"] & 1 else moved["qg_read"] + moved["qg_written"]) +
+                     (0 if st["fused"] & 2 else 2 * (moved["kg_read"] + moved["kg_written"]))) * D * 2,
+                    "(rows read + rows written) x D x 2 B of the materialised views (mmi_traffic_stats): "
+                    + ("Kbar, Vbar (Q gathered in the attention kernel)" if st["fused"] == 1 else
+                       "none (all gathered in the attention kernel)" if st["fused"] == 3 else "Qbar, Kbar, Vbar")),
         # LSE merge: two fp16 partial rows + two fp32 LSEs in, one bf16 row out, per token of a merged head
         "unpermute": (st["merge_heads"] * S * (2 * D * 2 + 2 * 4 + D * 2),
                       "merged heads x S x (2 fp16 partial rows + 2 fp32 LSE + 1 bf16 row)"),
     }
     hbm = {"peak_GBs": hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs", "stages": {}}
     for name, (nbytes, how) in alg.items():
-        gbs = nbytes / (stage[name] * 1e-3) / 1e9 if stage[name] > 0 else None
+        gbs = nbytes / (stage[name] * 1e-3) / 1e9 if stage[name] > 0 and nbytes > 0 else None
         hbm["stages"][name] = {"bytes": int(nbytes), "GBps": gbs, "frac": (gbs / hbm_peak) if gbs else None,
                                "bytes_def": how}
     est = estimate_bound(wl, lheads, S, D, float(peaks.get("sm_max_mhz", 1965.0)), peaks)
@@ -533,8 +539,8 @@ def main():
             "roofline": roof, "hbm": hbm, "estimate": est,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": count_launches(lheads) * args.steps,
-            "gpu_launches_per_step": count_launches(lheads),
+            "gpu_launches": count_launches(lheads, int(st["fused"])) * args.steps,
+            "gpu_launches_per_step": count_launches(lheads, int(st["fused"])),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

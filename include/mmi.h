@@ -122,8 +122,13 @@ MMI_API mmi_status mmi_estimate_index(const mmi_problem* problem, const mmi_head
                               const void* q, const void* k, const uint8_t* modality,
                               void* ws, size_t ws_bytes, mmi_stream_t stream);
 
-/* Step a6: gather the permuted Q̄ / K̄ / V̄ views the index needs into the
- * workspace (pads zero-filled).  Requires mmi_estimate_index on the same ws. */
+/* Step a6: the permutation of Q / K / V into the views the index needs (
+ * "dynamically loading and writing these tensors within the kernel").  Default build:
+ * permuted Q blocks are gathered by mmi_sparse_prefill itself (TMA row gathers from q; outputs are
+ * scattered by its epilogue), and this call materialises only K̄ / V̄, which many work items
+ * re-read (pads zero-filled).  -DMMI_FUSE_KV builds gather K / V in the kernel too (no copy at
+ * all); -DMMI_EXPLICIT_PERMUTE builds materialise Q̄ as well.  Requires mmi_estimate_index on the
+ * same ws. */
 MMI_API mmi_status mmi_permute(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws, size_t ws_bytes,
                        const void* q, const void* k, const void* v, mmi_stream_t stream);
 
@@ -147,7 +152,8 @@ MMI_API mmi_status mmi_dense_prefill(const mmi_problem* problem, const void* q, 
 /* Sizes of the plan for (problem, cfg_host), host-only (no device work), for
  * reporting algorithmic traffic: out[0] = gathered Q rows (Q̄), out[1] = gathered
  * K/V rows (K̄ and V̄ each), out[2] = heads with LSE-merged rows, out[3] = estimation
- * slabs, out[4] = partial-output rows.  Writes min(n, 5) values.  Returns
+ * slabs, out[4] = partial-output rows, out[5] = in-kernel permutation bits (1: permuted Q blocks
+ * are gathered by mmi_sparse_prefill, no Q̄ copy; 2: the same for K / V).  Writes min(n, 6) values.  Returns
  * MMI_E_INVALID / MMI_E_SHAPE / MMI_E_CONFIG like mmi_workspace_bytes' validation. */
 MMI_API mmi_status mmi_plan_stats(const mmi_problem* problem, const mmi_head_config* cfg_host, int64_t* out_host,
                                   int n);
@@ -169,6 +175,18 @@ MMI_API mmi_status mmi_export_index(const mmi_problem* problem, const mmi_head_c
 MMI_API mmi_status mmi_sparse_fingerprint(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws,
                                   size_t ws_bytes, const void* q, const void* k, const void* v, int64_t* fp,
                                   mmi_stream_t stream);
+
+/* ANALYSIS.  Top-k coverage: for every head h and sampled
+ * query row rows[i] (device int32 positions), the smallest number of keys whose causal softmax
+ * probabilities sum to at least `target` (e.g. 0.95 -> "top 5.78% of attention weights recall
+ * 95%"), divided by the row's causal key count rows[i] + 1; written to frac [H, n_rows]
+ * (device fp32).  Scratch (device) of mmi_topk_coverage_scratch_bytes(problem, n_rows) bytes.
+ * Asynchronous; deterministic (integer fixed-point mass histograms).  Returns MMI_E_INVALID /
+ * MMI_E_SHAPE / MMI_E_WORKSPACE on bad arguments, MMI_E_CUDA if a launch fails. */
+MMI_API size_t mmi_topk_coverage_scratch_bytes(const mmi_problem* problem, int32_t n_rows);
+MMI_API mmi_status mmi_topk_coverage(const mmi_problem* problem, const void* q, const void* k, const int32_t* rows,
+                                     int32_t n_rows, float target, float* frac, void* scratch, size_t scratch_bytes,
+                                     mmi_stream_t stream);
 
 /* DIAGNOSTIC (synchronises the stream).  Device-side error flags raised by the last
  * mmi_estimate_index on this workspace (0 = none):

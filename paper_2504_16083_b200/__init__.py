@@ -4,5 +4,5 @@ from .mmi import (  # noqa: F401
     SparsePrefill, HostSparsePrefill, dense_prefill, lib, MMIError,
     mmi_workspace_bytes, mmi_estimate_index, mmi_permute, mmi_sparse_prefill, mmi_unpermute,
     mmi_dense_prefill, mmi_export_index, mmi_sparse_fingerprint, mmi_plan_stats, mmi_traffic_stats,
-    mmi_workspace_flags,
+    mmi_workspace_flags, mmi_topk_coverage,
 )

@@ -224,9 +224,9 @@ extern "C" mmi_status mmi_plan_stats(const mmi_problem* pb, const mmi_head_confi
   const mmi_status st = prepare(pb, cfg, nullptr, 0, cp, false);
   if (st != MMI_OK) return st;
   const Plan& P = cp->P;
-  const int64_t v[5] = {P.qg_rows, P.kg_rows, (int64_t)P.merge_heads.size(), (int64_t)P.slabs.size(),
-                        (int64_t)P.part_rows};
-  for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
+  const int64_t v[6] = {P.qg_rows, P.kg_rows, (int64_t)P.merge_heads.size(), (int64_t)P.slabs.size(),
+                        (int64_t)P.part_rows, (int64_t)P.fused};
+  for (int i = 0; i < n && i < 6; ++i) out[i] = v[i];
   return MMI_OK;
 }
 
@@ -306,8 +306,10 @@ extern "C" mmi_status mmi_permute(const mmi_problem* pb, const mmi_head_config* 
   const Plan& P = cp->P;
   if (!q || !k || !v) return fail(MMI_E_INVALID, "null tensor pointer");
   cudaStream_t s = (cudaStream_t)stream;
-  launch_gather(at<int>(ws, P.qg_src), P.qg_rows, P.D, q, at<void>(ws, P.qg), nullptr, nullptr, s);
-  launch_gather(at<int>(ws, P.kg_src), P.kg_rows, P.D, k, at<void>(ws, P.kg), v, at<void>(ws, P.vg), s);
+  // permuted blocks the attention kernel does not gather itself (f2, plan.h FUSE_*) are materialised
+  if (!(P.fused & FUSE_Q)) launch_gather(at<int>(ws, P.qg_src), P.qg_rows, P.D, q, at<void>(ws, P.qg), nullptr, nullptr, s);
+  if (!(P.fused & FUSE_KV))
+    launch_gather(at<int>(ws, P.kg_src), P.kg_rows, P.D, k, at<void>(ws, P.kg), v, at<void>(ws, P.vg), s);
   CK(cudaGetLastError());
   return MMI_OK;
 }
@@ -341,6 +343,11 @@ static mmi_status run_sparse(const Plan& P, const mmi_problem* pb, void* ws, con
   A.dbg = g_dbg;
   A.fp_out = fp;
   A.sched = at<unsigned int>(ws, P.sched);
+  A.fused = P.fused;
+  A.qg_src = at<int>(ws, P.qg_src);
+  A.kg_src = at<int>(ws, P.kg_src);
+  A.q_oob = 0;   // padding rows gather row 0: finite values, masked (K) / never written (Q) / P = 0 (V)
+  A.kv_oob = 0;
   // partial rows of work items without a live tile are never written: NaN-fill their LSEs so the
   // merges of mmi_unpermute skip them (0xFF bytes = NaN)
   if (P.part_rows > 0) {

@@ -268,6 +268,21 @@ struct SegIter {
   }
 };
 
+// Warp-collective row gather of one 128-row block into the 128B-swizzled tile layout of TMA box
+// {64 columns, 128 rows}: lane l gathers rows 4l .. 4l+3 (source rows src[4l .. 4l+3]; negative =
+// padding -> the out-of-range row `oob`, zero-filled) for every 64-column block.
+template <int D>
+__device__ __forceinline__ void gather_rows_tma(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
+                                                const int32_t* src, int oob, int lane) {
+  int4 r = __ldg(reinterpret_cast<const int4*>(src) + lane);
+  r.x = r.x < 0 ? oob : r.x;
+  r.y = r.y < 0 ? oob : r.y;
+  r.z = r.z < 0 ? oob : r.z;
+  r.w = r.w < 0 ? oob : r.w;
+#pragma unroll
+  for (int c = 0; c < D / 64; ++c) tma_gather4(dst + c * (BLK * 128) + lane * 4 * 128, tm, bar, c * 64, r.x, r.y, r.z, r.w);
+}
+
 template <int D>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_kernel(const __grid_constant__ CUtensorMap tmQo, const __grid_constant__ CUtensorMap tmQg,
@@ -370,16 +385,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(CTRL_REGS));
     if (warp == 0) {
       // ======================= scheduler + Q loader =======================
-      if (elect_one()) {
-        uint32_t q_phase = 0, rs_phase = 0;
-        int rs = 0;
-        for (int i = 0;; ++i) {
-          const int slot = i % SCHED_RING;
+      // lane 0 schedules and stages; the whole warp issues the row gathers of permuted Q blocks
+      const bool leader = (lane == 0);
+      uint32_t q_phase = 0, rs_phase = 0;
+      int rs = 0;
+      for (int i = 0;; ++i) {
+        const int slot = i % SCHED_RING;
+        int idx = 0;
+        if (leader) {
           mbar_wait(sched_empty + slot, ((i / SCHED_RING) & 1) ^ 1);
           // dynamic fetch from the workspace counter; static round-robin without one (dense
           // comparator: its implicit items are already in longest-first order)
-          int idx = (i == 0) ? (int)blockIdx.x
-                             : (P.sched ? (int)gridDim.x + (int)atomicAdd(P.sched, 1u) : (int)blockIdx.x + i * (int)gridDim.x);
+          idx = (i == 0) ? (int)blockIdx.x
+                         : (P.sched ? (int)gridDim.x + (int)atomicAdd(P.sched, 1u) : (int)blockIdx.x + i * (int)gridDim.x);
           if (idx >= n_items) idx = -1;
           sched_ring[slot * (SCHED_ENTRY / 4)] = idx;
           if (idx >= 0 && !P.dense) {
@@ -389,9 +407,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int w = 0; w < (int)(sizeof(WorkItem) / 16); ++w) dst[w] = src[w];
           }
           mbar_arrive(sched_full + slot);
-          if (idx < 0) break;
-          const ItemView it = item_of(i, idx);
-          if (it.n_tiles <= 0) continue;
+        }
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        __syncwarp();
+        if (idx < 0) break;
+        const ItemView it = item_of(i, idx);
+        if (it.n_tiles <= 0) continue;
+        if (leader) {
           if (P.dbg) P.dbg[idx * 8 + 0] = gtimer();
           if (!P.dense) {
             // stage the rows' positions / ranks (contiguous slices) for the softmax warps
@@ -408,14 +430,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               mbar_arrive_expect_tx(ri_full + rs, n4 * 4);
               if (n4 > 0) bulk_load(rip + 2 * BLK, P.rank + x0, n4 * 4, ri_full + rs);
             }
-            if (++rs == 2) {
-              rs = 0;
-              rs_phase ^= 1;
-            }
           }
           mbar_wait(q_empty, q_phase ^ 1);
-          q_phase ^= 1;
           mbar_arrive_expect_tx(q_full, (it.has_b ? 2 : 1) * L::Q_BYTES);
+        }
+        if (!P.dense && ++rs == 2) {
+          rs = 0;
+          rs_phase ^= 1;
+        }
+        q_phase ^= 1;
+        __syncwarp();
+        if (it.q_gathered && (P.fused & 1)) {
+          // in-kernel permutation: the rows of a permuted Q block are gathered straight
+          // from Q (tile::gather4, 4 rows per lane and 64-column block)
+          for (int hf = 0; hf < (it.has_b ? 2 : 1); ++hf)
+            gather_rows_tma<D>(smem + L::OFF_Q + hf * L::Q_BYTES, &tmQg, q_full,
+                               P.qg_src + it.q_row0 + hf * BLK, P.q_oob, lane);
+        } else if (leader) {
           const CUtensorMap* tq = it.q_gathered ? &tmQg : &tmQo;
           for (int hf = 0; hf < (it.has_b ? 2 : 1); ++hf) {
 #pragma unroll
@@ -428,46 +459,57 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else if (warp == 2 || warp == 3) {
       // ======================= K loader (warp 2) / V loader (warp 3) =======================
       const bool is_k = (warp == 2);
-      if (elect_one()) {
-        int stage = 0, kps = 0;
-        uint32_t phase = 0, kp_phase = 0;
-        const int NS = is_k ? KST : VST;
-        uint64_t* full = is_k ? k_full : v_full;
-        uint64_t* empty = is_k ? k_empty : v_empty;
-        for (int i = 0;; ++i) {
-          const int idx = fetch(i);
-          mbar_arrive(sched_empty + i % SCHED_RING);
-          if (idx < 0) break;
-          const ItemView it = item_of(i, idx);
-          if (it.n_tiles <= 0) continue;
-          SegIter si;
-          si.init(P, it);
-          for (int t = 0; t < it.n_tiles; ++t) {
-            const TileInfo e = si.next(P, it);
+      const bool leader = (lane == 0);
+      int stage = 0, kps = 0;
+      uint32_t phase = 0, kp_phase = 0;
+      const int NS = is_k ? KST : VST;
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      for (int i = 0;; ++i) {
+        const int idx = fetch(i);
+        __syncwarp();
+        if (leader) mbar_arrive(sched_empty + i % SCHED_RING);
+        if (idx < 0) break;
+        const ItemView it = item_of(i, idx);
+        if (it.n_tiles <= 0) continue;
+        SegIter si;
+        si.init(P, it);
+        for (int t = 0; t < it.n_tiles; ++t) {
+          const TileInfo e = si.next(P, it);
+          uint8_t* dst = smem + (is_k ? L::OFF_K : L::OFF_V) + stage * L::KV_BYTES;
+          if (leader) {
             mbar_wait(empty + stage, phase ^ 1);
             if (is_k) live_s[stage] = (int)e.live();  // read by the MMA issuer after k_full (release: the arrive below)
             mbar_arrive_expect_tx(full + stage, L::KV_BYTES);
+          }
+          __syncwarp();
+          if (e.space && (P.fused & 2)) {
+            // in-kernel permutation (Alg.6 "Load index I_chip"): the tile's rows are
+            // gathered from the original K / V by their source rows (tile::gather4)
+            gather_rows_tma<D>(dst, is_k ? &tmKg : &tmVg, full + stage, P.kg_src + e.krow, P.kv_oob, lane);
+          } else if (leader) {
             const CUtensorMap* tm = is_k ? (e.space ? &tmKg : &tmKo) : (e.space ? &tmVg : &tmVo);
-            uint8_t* dst = smem + (is_k ? L::OFF_K : L::OFF_V) + stage * L::KV_BYTES;
 #pragma unroll
             for (int c = 0; c < D / 64; ++c) tma_load_2d(dst + c * (BLK * 128), tm, full + stage, c * 64, e.krow);
-            // key coordinates of gathered tiles the softmax masks or fingerprints (same predicate there)
-            const bool cp_pos = is_k && (e.pred_any() || P.fingerprint) && e.space;
-            if (cp_pos) {
+          }
+          // key coordinates of gathered tiles the softmax masks or fingerprints (same predicate there)
+          const bool cp_pos = is_k && (e.pred_any() || P.fingerprint) && e.space;
+          if (cp_pos) {
+            if (leader) {
               const bool cp_rank = e.pred_any() && e.rmode;
               mbar_wait(kp_empty + kps, kp_phase ^ 1);
               mbar_arrive_expect_tx(kp_full + kps, (cp_rank ? 2 : 1) * BLK * 4);
               bulk_load(kpos_s + kps * BLK, P.kg_pos + e.krow, BLK * 4, kp_full + kps);
               if (cp_rank) bulk_load(krank_s + kps * BLK, P.kg_rank + e.krow, BLK * 4, kp_full + kps);
-              if (++kps == NKP) {
-                kps = 0;
-                kp_phase ^= 1;
-              }
             }
-            if (++stage == NS) {
-              stage = 0;
-              phase ^= 1;
+            if (++kps == NKP) {
+              kps = 0;
+              kp_phase ^= 1;
             }
+          }
+          if (++stage == NS) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
@@ -1167,6 +1209,23 @@ int make_tmap_rows(CUtensorMap* m, const void* base, long long rows, int D) {
   return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
+// rows x D bf16 row-major tensor for tile::gather4: box = 64 columns x 1 row, 128B swizzle (each
+// gather4 lands 4 rows of 128 B; the swizzle follows the shared-memory address, so 32 gathers build
+// the same tile as one {64, 128} box load)
+static int make_tmap_gather(CUtensorMap* m, const void* base, long long rows, int D) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return -1;
+  if (rows <= 0) rows = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
 // rows x D 16-bit row-major output; box = 32 rows x 16 columns (32 B), 32B swizzle (epilogue staging)
 static int make_tmap_out(CUtensorMap* m, const void* base, long long rows, int D, CUtensorMapDataType dt) {
   PFN_encodeTiled enc = get_encode();
@@ -1188,11 +1247,21 @@ cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hi
   CUtensorMap m[8];
   int e = 0;
   e |= make_tmap_rows(&m[0], L.q, L.q_rows, P.D);
-  e |= make_tmap_rows(&m[1], L.qg ? L.qg : L.q, L.qg ? L.qg_rows : L.q_rows, P.D);
   e |= make_tmap_rows(&m[2], L.k, L.kv_rows, P.D);
-  e |= make_tmap_rows(&m[3], L.kg ? L.kg : L.k, L.kg ? L.kvg_rows : L.kv_rows, P.D);
   e |= make_tmap_rows(&m[4], L.v, L.kv_rows, P.D);
-  e |= make_tmap_rows(&m[5], L.vg ? L.vg : L.v, L.vg ? L.kvg_rows : L.kv_rows, P.D);
+  // permuted blocks: row-gather maps over the ORIGINAL tensors (in-kernel permutation, P.fused) or
+  // tile maps over the materialised Q̄ / K̄ / V̄
+  if (P.fused & 1)
+    e |= make_tmap_gather(&m[1], L.q, L.q_rows, P.D);
+  else
+    e |= make_tmap_rows(&m[1], L.qg ? L.qg : L.q, L.qg ? L.qg_rows : L.q_rows, P.D);
+  if (P.fused & 2) {
+    e |= make_tmap_gather(&m[3], L.k, L.kv_rows, P.D);
+    e |= make_tmap_gather(&m[5], L.v, L.kv_rows, P.D);
+  } else {
+    e |= make_tmap_rows(&m[3], L.kg ? L.kg : L.k, L.kg ? L.kvg_rows : L.kv_rows, P.D);
+    e |= make_tmap_rows(&m[5], L.vg ? L.vg : L.v, L.vg ? L.kvg_rows : L.kv_rows, P.D);
+  }
   // output maps (epilogue TMA stores): bf16 O [H*S, D] and fp16 partial rows [part_rows, D]
   e |= make_tmap_out(&m[6], P.o ? P.o : L.q, P.o ? L.o_rows : L.q_rows, P.D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
   e |= make_tmap_out(&m[7], L.part_rows > 0 ? (const void*)P.part_o : L.q, L.part_rows > 0 ? L.part_rows : L.q_rows,

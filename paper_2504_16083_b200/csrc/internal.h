@@ -107,10 +107,18 @@ struct AttnParams {
   int64_t* fp_out;          // [H, S, 3] count, sum pos, sum pos^2 (fingerprint mode)
   long long* dbg;           // optional per-item timestamps (debug only)
   unsigned int* sched;      // work-item counter (zeroed before the launch)
+  // in-kernel permutation: permuted Q / K / V blocks are gathered from the
+  // original tensors by their source rows (TMA tile::gather4) instead of reading materialised
+  // Q̄ / K̄ / V̄ copies
+  int32_t fused;            // bit 0: gather permuted Q blocks from q; bit 1: K / V blocks from k / v
+  const int32_t* qg_src;    // Q̄ row -> row of Q [H*S] (negative: padding)
+  const int32_t* kg_src;    // K̄ row -> row of K / V [Hkv*S] (negative: padding)
+  int32_t q_oob, kv_oob;    // out-of-range row (zero fill) of Q / of K and V
 };
 
 struct AttnLaunch {
-  const void *q, *qg, *k, *kg, *v, *vg;   // original and gathered Q/K/V spaces (bf16 rows of D)
+  const void *q, *qg, *k, *kg, *v, *vg;   // original and gathered Q/K/V spaces (bf16 rows of D); fused:
+                                          // qg / kg / vg unused, the gather maps cover q / k / v
   long long q_rows, qg_rows, kv_rows, kvg_rows;
   long long o_rows = 0, part_rows = 0;   // rows of the bf16 output [H*S] and of the fp16 partial buffer
 };

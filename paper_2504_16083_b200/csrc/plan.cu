@@ -499,9 +499,14 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
   reg(P.kg_pos, sizeof(int) * P.kg_rows);
   reg(P.kg_rank, sizeof(int) * P.kg_rows);
   reg(P.kg_src, sizeof(int) * P.kg_rows);
-  reg(P.qg, (size_t)P.qg_rows * P.D * 2);
-  reg(P.kg, (size_t)P.kg_rows * P.D * 2);
-  reg(P.vg, (size_t)P.kg_rows * P.D * 2);
+#if defined(MMI_EXPLICIT_PERMUTE)
+  P.fused = 0;  // mmi_permute materialises Q̄ / K̄ / V̄ (the round-1 path, kept for A/B measurement)
+#elif defined(MMI_FUSE_KV)
+  P.fused = FUSE_Q | FUSE_KV;
+#endif
+  reg(P.qg, (P.fused & FUSE_Q) ? 0 : (size_t)P.qg_rows * P.D * 2);
+  reg(P.kg, (P.fused & FUSE_KV) ? 0 : (size_t)P.kg_rows * P.D * 2);
+  reg(P.vg, (P.fused & FUSE_KV) ? 0 : (size_t)P.kg_rows * P.D * 2);
   reg(P.items, sizeof(WorkItem) * P.n_slots);
   reg(P.items_sorted, sizeof(WorkItem) * P.n_slots);
   reg(P.item_keys, sizeof(int) * 2 * (size_t)P.n_slots);

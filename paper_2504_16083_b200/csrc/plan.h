@@ -19,9 +19,9 @@ constexpr int FOLD_GAP = 128;    // reading C6
 constexpr int SLAB_ROWS = 64;    // max last_q
 constexpr int SLAB_CHUNK = 1024; // keys per slab CTA (8 tiles)
 #ifndef MMI_HROW_SPLIT
-#define MMI_HROW_SPLIT 128
+#define MMI_HROW_SPLIT 512
 #endif
-constexpr int HROW_SPLIT_TILES = MMI_HROW_SPLIT;  // split-K chunk of an h-line row pair (16384 keys)
+constexpr int HROW_SPLIT_TILES = MMI_HROW_SPLIT;  // split-K chunk of an h-line row pair (65536 keys)
 
 enum PassKind : int32_t { PASS_MAIN = 0, PASS_HROW = 1, PASS_SLASH = 2 };
 enum ViewKind : int32_t { VK_ORIG_CLASS = 0, VK_RANK_CLASS = 1, VK_MOD = 2, VK_VCOL = 3 };
@@ -76,6 +76,8 @@ struct GridRes {
   double J, T;
 };
 
+constexpr int FUSE_Q = 1, FUSE_KV = 2;
+
 struct Region {
   size_t off = 0, bytes = 0;
 };
@@ -127,6 +129,12 @@ struct Plan {
   Region items, item_keys, item_vals, items_sorted, seg_cnt, seg_off, segs, inst_params, sort_tmp, scan_tmp;
   Region part_o, part_lse;
   Region sched, flags;
+  // in-kernel permutation (f2), bit 0: permuted Q blocks gathered by the attention kernel (no Q̄
+  // copy); bit 1: the same for K / V (no K̄ / V̄).  Default: Q only -- a K̄ / V̄ tile is re-read by
+  // many work items (a grid head's vertical strip by every row block), so one coalesced
+  // materialisation that stays in L2 beats re-gathering scattered rows from K / V each time
+  // (measured: DESIGN.md §6.3)
+  int fused = FUSE_Q;
   size_t total = 0;
 };
 

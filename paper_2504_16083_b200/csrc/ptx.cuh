@@ -88,6 +88,17 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* d
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// TMA row gather (sm_100): 4 rows r0..r3 x box-inner columns starting at column c0 of a 2D tensor
+// map whose box is {inner, 1}; the rows land consecutively at smem_dst (swizzle by smem address).
+// Out-of-range rows are zero-filled.
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* desc, uint64_t* bar, int32_t c0,
+                                            int32_t r0, int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6, %7}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
 // TMA tensor store shared -> global (bulk-group completion)
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* desc, uint32_t smem_src, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(

@@ -71,11 +71,14 @@ def lib():
         L.mmi_plan_stats.argtypes = [P, C, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         L.mmi_traffic_stats.argtypes = [P, C, vp, sz, ctypes.POINTER(ctypes.c_int64), vp]
         L.mmi_workspace_flags.argtypes = [P, C, vp, sz, ctypes.POINTER(ctypes.c_uint32), vp]
+        L.mmi_topk_coverage_scratch_bytes.restype = sz
+        L.mmi_topk_coverage_scratch_bytes.argtypes = [P, i32]
+        L.mmi_topk_coverage.argtypes = [P, vp, vp, vp, i32, ctypes.c_float, vp, vp, sz, vp]
         L.mmi_last_error.restype = ctypes.c_char_p
         L.mmi_version.restype = ctypes.c_char_p
         for fn in ("mmi_estimate_index", "mmi_permute", "mmi_sparse_prefill", "mmi_unpermute",
                    "mmi_dense_prefill", "mmi_export_index", "mmi_sparse_fingerprint", "mmi_plan_stats",
-                   "mmi_traffic_stats", "mmi_workspace_flags"):
+                   "mmi_traffic_stats", "mmi_workspace_flags", "mmi_topk_coverage"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -155,9 +158,9 @@ def mmi_workspace_bytes(pb: Problem, cfgs: Sequence[HeadConfig]) -> int:
 
 def mmi_plan_stats(pb: Problem, cfgs: Sequence[HeadConfig]) -> dict:
     """Host-only plan sizes (for algorithmic-traffic reporting)."""
-    out = (ctypes.c_int64 * 5)()
-    _check(lib().mmi_plan_stats(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), out, 5))
-    return dict(qg_rows=out[0], kg_rows=out[1], merge_heads=out[2], slabs=out[3], part_rows=out[4])
+    out = (ctypes.c_int64 * 6)()
+    _check(lib().mmi_plan_stats(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), out, 6))
+    return dict(qg_rows=out[0], kg_rows=out[1], merge_heads=out[2], slabs=out[3], part_rows=out[4], fused=out[5])
 
 
 def mmi_traffic_stats(pb: Problem, cfgs: Sequence[HeadConfig], ws, stream=None) -> dict:
@@ -218,6 +221,22 @@ def mmi_workspace_flags(pb, cfgs, ws, stream=None) -> int:
     _check(lib().mmi_workspace_flags(ctypes.byref(to_c_problem(pb)), to_c_configs(cfgs), _ptr(ws),
                                      ws.numel() * ws.element_size(), ctypes.byref(f), _stream(stream)))
     return int(f.value)
+
+
+def mmi_topk_coverage(pb, q, k, rows, target=0.95, stream=None) -> torch.Tensor:
+    """ANALYSIS: [H, n_rows] fraction of causal keys whose top mass reaches `target` (C ABI)."""
+    _need_cuda(q, k, rows)
+    _check_io(pb, q=q, k=k)
+    if rows.dtype != torch.int32:
+        raise TypeError("mmi: rows must be int32")
+    n = rows.numel()
+    out = torch.empty((pb.n_heads, n), dtype=torch.float32, device=q.device)
+    c_pb = to_c_problem(pb)
+    nb = int(lib().mmi_topk_coverage_scratch_bytes(ctypes.byref(c_pb), n))
+    scratch = torch.empty(nb, dtype=torch.uint8, device=q.device)
+    _check(lib().mmi_topk_coverage(ctypes.byref(c_pb), _ptr(q), _ptr(k), _ptr(rows), n, float(target), _ptr(out),
+                                   _ptr(scratch), nb, _stream(stream)))
+    return out
 
 
 def mmi_export_index(pb, cfgs, ws, head: int, stream=None) -> torch.Tensor:

@@ -151,3 +151,71 @@ class Problem:
     @property
     def tau(self) -> float:
         return self.scale if self.scale > 0 else 1.0 / (self.head_dim ** 0.5)
+
+
+# ---------------------------------------------------------------- JSON head-config contract
+# The offline search (Alg.4) persists one entry per head; the runtime path reads it back
+# ("HeadConfig table persisted as JSON").  Pure data, no arithmetic.
+import json as _json
+from dataclasses import asdict as _asdict, fields as _fields
+
+BND_BY_NAME = {v: k for k, v in BND_NAMES.items()}
+
+
+def pattern_to_dict(p: Pattern) -> dict:
+    d = _asdict(p)
+    d["kind"] = KIND_NAMES[p.kind]
+    return d
+
+
+def pattern_from_dict(d: dict) -> Pattern:
+    kinds = {v: k for k, v in KIND_NAMES.items()}
+    d = dict(d)
+    d["kind"] = kinds[d["kind"]] if isinstance(d["kind"], str) else int(d["kind"])
+    names = {f.name for f in _fields(Pattern)}
+    return Pattern(**{k: v for k, v in d.items() if k in names})
+
+
+def head_config_to_dict(c: HeadConfig, head_id: int = 0, **extra) -> dict:
+    d = {"head_id": head_id, "boundary": BND_NAMES[c.boundary]}
+    if c.boundary in (BND_NONE, BND_K):
+        d["intra"] = {"0": pattern_to_dict(c.intra[0])}
+    elif c.boundary == BND_Q:
+        d["intra"] = {str(m): pattern_to_dict(p) for m, p in enumerate(c.intra) if p.kind != KIND_NONE}
+    else:
+        d["pair"] = {f"{a},{b}": pattern_to_dict(c.pair[a][b]) for a in range(MAX_MOD) for b in range(MAX_MOD)
+                     if c.pair[a][b].kind != KIND_NONE}
+    d.update(extra)
+    return d
+
+
+def head_config_from_dict(d: dict) -> HeadConfig:
+    b = BND_BY_NAME[d["boundary"]]
+    if b in (BND_NONE, BND_K):
+        c = HeadConfig.no_boundary(pattern_from_dict(d["intra"]["0"]))
+        c.boundary = b
+        return c
+    if b == BND_Q:
+        intra = [none()] * MAX_MOD
+        for m, p in d["intra"].items():
+            intra[int(m)] = pattern_from_dict(p)
+        return HeadConfig(boundary=BND_Q, intra=intra)
+    pr = [[none()] * MAX_MOD for _ in range(MAX_MOD)]
+    for key, p in d.get("pair", {}).items():
+        a, bb = (int(x) for x in key.split(","))
+        pr[a][bb] = pattern_from_dict(p)
+    return HeadConfig(boundary=BND_2D, pair=pr)
+
+
+def save_head_configs(path: str, cfgs: List[HeadConfig], meta: Optional[dict] = None,
+                      per_head: Optional[List[dict]] = None) -> None:
+    heads = [head_config_to_dict(c, h, **((per_head or [{}] * len(cfgs))[h])) for h, c in enumerate(cfgs)]
+    with open(path, "w") as f:
+        _json.dump({"meta": meta or {}, "heads": heads}, f, indent=1, sort_keys=True)
+
+
+def load_head_configs(path: str) -> List[HeadConfig]:
+    with open(path) as f:
+        d = _json.load(f)
+    heads = sorted(d["heads"], key=lambda x: x["head_id"])
+    return [head_config_from_dict(h) for h in heads]
