@@ -78,7 +78,7 @@ def count_launches(heads, fused: int = 1) -> int:
     if any(p.kind in (KIND_GRID, KIND_VSLASH) for p in pats):
         n += 4                              # slab rows, pass 1, combine, pass 2
     if any(p.kind == KIND_GRID for p in pats) or static:
-        n += 4                              # gather-rank, fold, eval, pick
+        n += 5                              # gather-rank, fold, derive, eval, pick
     if any(p.kind == KIND_VSLASH for p in pats):
         n += 1                              # vs select
     n += 2 + 1 + 1                          # views (Q, K), inst params, items count

@@ -176,6 +176,32 @@ MMI_API mmi_status mmi_sparse_fingerprint(const mmi_problem* problem, const mmi_
                                   size_t ws_bytes, const void* q, const void* k, const void* v, int64_t* fp,
                                   mmi_stream_t stream);
 
+/* Permuted NATTEN / DiT neighborhood attention (App. F): tokens of a
+ * T x Hh x Ww grid in raster order (pos = (t * Hh + y) * Ww + x, T * Hh * Ww = seq_len); every
+ * query attends BIDIRECTIONALLY to the kt x kh x kw window around it, clamped inside the grid
+ * (start = clamp(c - k/2, 0, L - k) per dimension, NATTEN semantics, reading C25).  The tokens are
+ * permuted into bt x bh x bw = 128-token tiles so the windows become block-sparse tile lists run
+ * by the same tcgen05 kernel.  q [H,S,D], k/v [Hkv,S,D], o [H,S,D] bf16, lse [H,S] fp32 (nullable).
+ * The index depends only on (problem, config): built on the host once, cached, uploaded
+ * asynchronously from pinned memory.  Errors: MMI_E_SHAPE (T*Hh*Ww != S, H % Hkv, D),
+ * MMI_E_CONFIG (window > grid extent, tile != 128 tokens), MMI_E_WORKSPACE; message via
+ * mmi_natten_last_error(). */
+typedef struct {
+  int32_t T, Hh, Ww;   /* token grid */
+  int32_t kt, kh, kw;  /* window */
+  int32_t bt, bh, bw;  /* permutation tile, bt * bh * bw = 128 */
+} mmi_natten_config;
+MMI_API size_t mmi_natten_workspace_bytes(const mmi_problem* problem, const mmi_natten_config* cfg);
+MMI_API mmi_status mmi_natten_prefill(const mmi_problem* problem, const mmi_natten_config* cfg, void* ws,
+                                      size_t ws_bytes, const void* q, const void* k, const void* v, void* o,
+                                      float* lse, mmi_stream_t stream);
+/* TEST ONLY: per-row admitted-key fingerprints (count, sum pos, sum pos^2) as the kernel applies
+ * the window, int64 [H, S, 3] device buffer zeroed by the caller. */
+MMI_API mmi_status mmi_natten_fingerprint(const mmi_problem* problem, const mmi_natten_config* cfg, void* ws,
+                                          size_t ws_bytes, const void* q, const void* k, const void* v, int64_t* fp,
+                                          mmi_stream_t stream);
+MMI_API const char* mmi_natten_last_error(void);
+
 /* ANALYSIS.  Top-k coverage: for every head h and sampled
  * query row rows[i] (device int32 positions), the smallest number of keys whose causal softmax
  * probabilities sum to at least `target` (e.g. 0.95 -> "top 5.78% of attention weights recall

@@ -214,6 +214,30 @@ __device__ __forceinline__ void bit_window(const uint32_t* bits, int lo, uint32_
   for (int i = 0; i < 4; ++i) out[i] = __funnelshift_r(w[i], w[i + 1], sh);
 }
 
+// 128-bit admitted-key mask of a permuted NATTEN key tile for the query at raster position xpos:
+// per dimension the window [start, start + k) with start = clamp(c - k/2, 0, L - k) (reading C25),
+// intersected with the tile's local coordinates; key bit (lt * bh + ly) * bw + lx.
+__device__ __forceinline__ void natten_mask(const AttnParams& P, int xpos, int krow, uint32_t (&mw)[4]) {
+  const int HW = P.nat_H * P.nat_W;
+  const int qt = xpos / HW, qy = (xpos / P.nat_W) % P.nat_H, qx = xpos % P.nat_W;
+  const int st = min(max(qt - P.nat_kt / 2, 0), P.nat_T - P.nat_kt);
+  const int sy = min(max(qy - P.nat_kh / 2, 0), P.nat_H - P.nat_kh);
+  const int sx = min(max(qx - P.nat_kw / 2, 0), P.nat_W - P.nat_kw);
+  const int tile = (krow / BLK) % P.nat_tiles;
+  const int nX = (P.nat_W + P.nat_bw - 1) / P.nat_bw, nY = (P.nat_H + P.nat_bh - 1) / P.nat_bh;
+  const int TX = tile % nX, TY = (tile / nX) % nY, TT = tile / (nX * nY);
+  // local admitted ranges [lo, hi) per dimension
+  const int t0 = max(st - TT * P.nat_bt, 0), t1 = min(st + P.nat_kt - TT * P.nat_bt, P.nat_bt);
+  const int y0 = max(sy - TY * P.nat_bh, 0), y1 = min(sy + P.nat_kh - TY * P.nat_bh, P.nat_bh);
+  const int x0 = max(sx - TX * P.nat_bw, 0), x1 = min(sx + P.nat_kw - TX * P.nat_bw, P.nat_bw);
+  if (t1 <= t0 || y1 <= y0 || x1 <= x0) return;
+  for (int lt = t0; lt < t1; ++lt)
+    for (int ly = y0; ly < y1; ++ly) {
+      const int b = (lt * P.nat_bh + ly) * P.nat_bw;
+      range_mask(mw, b + x0, b + x1 - 1);
+    }
+}
+
 struct TileInfo {
   int krow;
   uint32_t space, role, rmode, inst;
@@ -839,6 +863,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int kbase = e.krow - kv * P.S;
             if (!pred) {
               range_mask(mw, 0, BLK - 1);
+            } else if (role == R_NAT) {
+              natten_mask(P, xpos, e.krow, mw);
             } else {
               if (!P.dense && role != R_TRUE && (int)inst != c_inst) {
                 // pattern parameters of the tile's instance: reloaded only when the instance changes

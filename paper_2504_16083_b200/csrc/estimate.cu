@@ -594,7 +594,10 @@ __global__ void __launch_bounds__(FOLD_THREADS) grid_acc_kernel(const DInst* __r
   const int gi = blockIdx.y;
   const DInst x = insts[grid_inst[gi]];
   if (x.stat) return;  // static grid: nothing to fold
-  const int s0 = x.smin + blockIdx.x * FOLD_SPC;
+  // only the strides without a candidate multiple are folded directly (s > smax / 2); the others
+  // are derived exactly from a power-of-two multiple by grid_derive_kernel
+  const int s_dir = max(x.smin, x.smax / 2 + 1);
+  const int s0 = s_dir + blockIdx.x * FOLD_SPC;
   if (s0 > x.smax) return;
   const int ns = min(FOLD_SPC, x.smax - s0 + 1);
   int lo, hi, n;
@@ -685,6 +688,31 @@ __global__ void __launch_bounds__(FOLD_THREADS) grid_acc_kernel(const DInst* __r
         if (p < s) gs[p] = accr[q][w];
       }
     }
+  }
+}
+
+// m_s[p] for s < s_dir from the direct fold of its multiple L = s * 2^k in (smax / 2, smax]:
+// j = p (mod s)  <=>  j mod L in {p, p + s, ..., p + (2^k - 1) s}, so m_s[p] = sum_i m_L[p + i s]
+// (exact integer sums, fixed order)
+__global__ void __launch_bounds__(256) grid_derive_kernel(const DInst* __restrict__ insts,
+                                                          const int* __restrict__ grid_inst,
+                                                          const int64_t* __restrict__ acc_off,
+                                                          uint32_t* __restrict__ acc) {
+  const int gi = blockIdx.y;
+  const DInst x = insts[grid_inst[gi]];
+  if (x.stat) return;
+  const int s_dir = max(x.smin, x.smax / 2 + 1);
+  const int s = x.smin + blockIdx.x;
+  if (s >= s_dir) return;
+  int L = s;
+  while (2 * L <= x.smax) L *= 2;
+  uint32_t* g = acc + acc_off[gi];
+  const uint32_t* mL = g + (size_t)(L - x.smin) * x.smax;
+  uint32_t* ms = g + (size_t)(s - x.smin) * x.smax;
+  for (int p = threadIdx.x; p < s; p += blockDim.x) {
+    uint32_t t = 0;
+    for (int q = p; q < L; q += s) t += mL[q];
+    ms[p] = t;
   }
 }
 
@@ -807,6 +835,7 @@ void launch_grid(const DInst* insts, const int* grid_inst, int n_grid, int max_n
   cudaFuncSetAttribute(grid_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fold_smem);
   grid_acc_kernel<<<dim3(n_sg, n_grid), FOLD_THREADS, fold_smem, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S,
                                                                 S_pad, acc_off, acc);
+  grid_derive_kernel<<<dim3(max_ncand, n_grid), 256, 0, st>>>(insts, grid_inst, acc_off, acc);
   grid_eval_kernel<<<dim3(max_ncand, n_grid), 256, 0, st>>>(insts, grid_inst, sinfo, info, S, acc_off, acc, part, res);
   grid_pick_kernel<<<n_grid, 1024, 0, st>>>(insts, grid_inst, part, res);
 }

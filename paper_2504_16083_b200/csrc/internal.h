@@ -24,7 +24,8 @@ constexpr unsigned FLAG_SEG_OVERFLOW = 2u;  // the index needed more tile segmen
 // admitted).  Per half the segment's tiles read
 //     DEAD^dh  PRED^ph  FULL*  PRED^pt  DEAD^dt      (st[half] = {dh, ph, pt, dt})
 // and a tile is in the segment only if it is live for at least one half.
-enum Role : uint32_t { R_TRUE = 0, R_A = 1, R_NOTA = 2, R_VSSL = 3 };
+// R_NAT: 3D neighborhood window of a permuted NATTEN tile (f4), bidirectional
+enum Role : uint32_t { R_TRUE = 0, R_A = 1, R_NOTA = 2, R_VSSL = 3, R_NAT = 4 };
 enum TileState : uint32_t { TS_DEAD = 0, TS_PRED = 1, TS_FULL = 2 };
 constexpr int SEG_MAX_TILES = 32767;   // per-half counts are int16
 struct Seg {
@@ -114,6 +115,9 @@ struct AttnParams {
   const int32_t* qg_src;    // Q̄ row -> row of Q [H*S] (negative: padding)
   const int32_t* kg_src;    // K̄ row -> row of K / V [Hkv*S] (negative: padding)
   int32_t q_oob, kv_oob;    // out-of-range row (zero fill) of Q / of K and V
+  // permuted NATTEN (f4): grid T x Hh x Ww, window kt x kh x kw, tiles bt x bh x bw (= 128 keys),
+  // nat_tiles tiles per head in the permuted K̄ space
+  int32_t nat_T, nat_H, nat_W, nat_kt, nat_kh, nat_kw, nat_bt, nat_bh, nat_bw, nat_tiles;
 };
 
 struct AttnLaunch {

@@ -42,6 +42,10 @@ class c_head_config(ctypes.Structure):
                 ("pair", (c_pattern * MAX_MOD) * MAX_MOD)]
 
 
+class c_natten_config(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("T", "Hh", "Ww", "kt", "kh", "kw", "bt", "bh", "bw")]
+
+
 class c_problem(ctypes.Structure):
     _fields_ = [("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32), ("seq_len", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("n_modalities", ctypes.c_int32), ("last_q", ctypes.c_int32),
@@ -71,6 +75,14 @@ def lib():
         L.mmi_plan_stats.argtypes = [P, C, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         L.mmi_traffic_stats.argtypes = [P, C, vp, sz, ctypes.POINTER(ctypes.c_int64), vp]
         L.mmi_workspace_flags.argtypes = [P, C, vp, sz, ctypes.POINTER(ctypes.c_uint32), vp]
+        NC = ctypes.POINTER(c_natten_config)
+        L.mmi_natten_workspace_bytes.restype = sz
+        L.mmi_natten_workspace_bytes.argtypes = [P, NC]
+        L.mmi_natten_prefill.argtypes = [P, NC, vp, sz, vp, vp, vp, vp, vp, vp]
+        L.mmi_natten_fingerprint.argtypes = [P, NC, vp, sz, vp, vp, vp, vp, vp]
+        L.mmi_natten_prefill.restype = ctypes.c_int
+        L.mmi_natten_fingerprint.restype = ctypes.c_int
+        L.mmi_natten_last_error.restype = ctypes.c_char_p
         L.mmi_topk_coverage_scratch_bytes.restype = sz
         L.mmi_topk_coverage_scratch_bytes.argtypes = [P, i32]
         L.mmi_topk_coverage.argtypes = [P, vp, vp, vp, i32, ctypes.c_float, vp, vp, sz, vp]
@@ -388,3 +400,37 @@ class HostSparsePrefill:
             done.record(st)
             caller.wait_event(done)
         return o_h
+
+
+class NattenPrefill:
+    """Permuted NATTEN / DiT neighborhood attention: owns the workspace; each call
+    runs mmi_natten_prefill on the current stream."""
+
+    def __init__(self, pb: Problem, nc, device="cuda"):
+        self.pb, self.nc = pb, nc
+        self.c_pb = to_c_problem(pb)
+        self.c_nc = c_natten_config(nc.T, nc.Hh, nc.Ww, nc.kt, nc.kh, nc.kw, nc.bt, nc.bh, nc.bw)
+        nbytes = int(lib().mmi_natten_workspace_bytes(ctypes.byref(self.c_pb), ctypes.byref(self.c_nc)))
+        if nbytes == 0:
+            raise MMIError(3, lib().mmi_natten_last_error().decode())
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+    def _st(self, st):
+        if st != MMI_OK:
+            raise MMIError(st, lib().mmi_natten_last_error().decode())
+
+    def __call__(self, q, k, v, o=None, lse=None, stream=None):
+        pb = self.pb
+        _need_cuda(q, k, v, o, lse)
+        _check_io(pb, q=q, k=k, v=v, o=o, lse=lse)
+        if o is None:
+            o = torch.empty((pb.n_heads, pb.seq_len, pb.head_dim), dtype=torch.bfloat16, device=q.device)
+        self._st(lib().mmi_natten_prefill(ctypes.byref(self.c_pb), ctypes.byref(self.c_nc), _ptr(self.ws),
+                                          self.ws.numel(), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                                          _stream(stream)))
+        return o
+
+    def fingerprint(self, q, k, v, fp, stream=None):
+        _need_cuda(q, k, v, fp)
+        self._st(lib().mmi_natten_fingerprint(ctypes.byref(self.c_pb), ctypes.byref(self.c_nc), _ptr(self.ws),
+                                              self.ws.numel(), _ptr(q), _ptr(k), _ptr(v), _ptr(fp), _stream(stream)))

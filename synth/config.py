@@ -219,3 +219,25 @@ def load_head_configs(path: str) -> List[HeadConfig]:
         d = _json.load(f)
     heads = sorted(d["heads"], key=lambda x: x["head_id"])
     return [head_config_from_dict(h) for h in heads]
+
+
+# ---------------------------------------------------------------- permuted NATTEN / DiT
+@dataclass(frozen=True)
+class NattenConfig:
+    """3D neighborhood (sliding-window) attention over a T x Hh x Ww token grid in raster order
+    (App. F: "the 2D/3D sliding window attention in NATTEN can be converted into dense
+    tensor core computation via permutation").  Window kt x kh x kw, clamped inside the grid
+    (NATTEN semantics, reading C25); tiles bt x bh x bw of 128 tokens define the permutation."""
+    T: int
+    Hh: int
+    Ww: int
+    kt: int
+    kh: int
+    kw: int
+    bt: int = 2
+    bh: int = 8
+    bw: int = 8
+
+    @property
+    def seq_len(self) -> int:
+        return self.T * self.Hh * self.Ww
