@@ -276,6 +276,77 @@ def plan_ranks(pb, heads, N, dist=None, dev=None, d=None, kv_range=None):
     return all_ranges(H, Hkv, N, cost), cost
 
 
+def bench_natten(args, rank, local, N):
+    """f4 workload (--workload 6): one permuted-NATTEN DiT layer (mmi_natten_prefill), heads sharded
+    across ranks (N > 1: each rank its head slice, no collective -- the output stays sharded)."""
+    import paper_2504_16083_b200 as mmi
+    from synth.workloads import natten_workload
+    name, pb0, nc = natten_workload()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    h0, h1 = rank * pb0.n_heads // N, (rank + 1) * pb0.n_heads // N
+    pb = Problem(h1 - h0, h1 - h0, pb0.seq_len, pb0.head_dim)
+    g = torch.Generator().manual_seed(args.seed + rank)
+    S, D = pb.seq_len, pb.head_dim
+    q = torch.randn(pb.n_heads, S, D, generator=g).to(torch.bfloat16).to(dev)
+    k = torch.randn(pb.n_kv_heads, S, D, generator=g).to(torch.bfloat16).to(dev)
+    v = torch.randn(pb.n_kv_heads, S, D, generator=g).to(torch.bfloat16).to(dev)
+    npf = mmi.NattenPrefill(pb, nc, device=dev)
+    o = torch.empty_like(q)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        npf(q, k, v, o)
+    torch.cuda.synchronize()
+    fp = torch.zeros((pb.n_heads, S, 3), dtype=torch.int64, device=dev)
+    npf.fingerprint(q, k, v, fp)
+    admitted = int(fp[:, :, 0].sum().item())
+    del fp
+    clocks = ClockSampler(local)
+    clocks.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        npf(q, k, v, o)
+    b.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = a.elapsed_time(b) / args.steps
+    if N > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    # same-build dense comparator: the same kernel with the window = the whole grid (every tile FULL)
+    from synth.config import NattenConfig
+    dn = mmi.NattenPrefill(pb, NattenConfig(nc.T, nc.Hh, nc.Ww, nc.T, nc.Hh, nc.Ww, nc.bt, nc.bh, nc.bw), device=dev)
+    dn(q, k, v, o)
+    torch.cuda.synchronize()
+    a.record(stream)
+    dn(q, k, v, o)
+    b.record(stream)
+    torch.cuda.synchronize()
+    dense_ms = a.elapsed_time(b)
+    peaks = _peaks()
+    # computed tiles: live (tile, half) pairs of the index = admitted keys rounded up to whole tiles;
+    # reported with the admitted-element FLOPs
+    achieved_adm = 4 * D * admitted / (ms * 1e-3) / 1e12
+    if rank == 0:
+        print(json.dumps({
+            "metric": "permuted NATTEN (DiT 3D neighborhood attention) ms/layer", "value": ms, "unit": UNIT,
+            "n_gpus": N, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn Q/K/V)",
+            "config": {"workload": name, "seq_len": S, "heads": pb0.n_heads, "head_dim": D,
+                       "grid": [nc.T, nc.Hh, nc.Ww], "window": [nc.kt, nc.kh, nc.kw], "tile": [nc.bt, nc.bh, nc.bw]},
+            "dense_ms": dense_ms, "speedup_vs_dense": dense_ms / ms,
+            "roofline": {"bound": "tensor", "achieved": achieved_adm, "peak": float(peaks["bf16_tflops"]),
+                         "unit": "TFLOP/s", "frac": achieved_adm / float(peaks["bf16_tflops"]), "traffic": None,
+                         "def": "admitted-element FLOPs 4*D*sum_i |window(i)| / mmi_natten_prefill time",
+                         "admitted_elements": admitted},
+            "gpu_launches": 4 * args.steps, "clocks": clk}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -296,7 +367,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     N = max(world, 1)
-    wl = build_workload(args.workload)
+    if args.workload == 6:
+        return bench_natten(args, rank, local, N)
+    if args.workload == 5:
+        from synth.workloads import baselines_workload
+        wl = baselines_workload()
+    else:
+        wl = build_workload(args.workload)
     pb = wl.problem
 
     if args.impl == "reference":

@@ -134,8 +134,9 @@ MMI_API mmi_status mmi_permute(const mmi_problem* problem, const mmi_head_config
 
 /* Step a7: block-sparse causal attention over every work item of the index
  * (tcgen05 / TMEM / TMA kernel).  Rows owned by a single pass are written to
- * o / lse directly; rows with several passes leave fp32 partials in ws.
- * lse may be NULL. */
+ * o / lse directly; rows with several passes (grid MAIN + SLASH, split-K h-line
+ * chunks) leave fp16 normalised partial rows + fp32 LSEs in ws (reading C22:
+ * requires |v| <= 65504, the fp16 range, since |O| <= max |v|).  lse may be NULL. */
 MMI_API mmi_status mmi_sparse_prefill(const mmi_problem* problem, const mmi_head_config* cfg_host, void* ws,
                               size_t ws_bytes, const void* q, const void* k, const void* v, void* o, float* lse,
                               mmi_stream_t stream);

@@ -63,8 +63,8 @@ constexpr int NWARP_SOFT = 8;                      // 2 softmax warpgroups: one 
 constexpr int NTHREADS = 32 * (NWARP_CTRL + NWARP_SOFT);
 constexpr int LAUNCH_REGS = 168;                   // ptxas allocation at __launch_bounds__(384, 1)
 #ifndef MMI_CTRL_REGS
-#define MMI_CTRL_REGS 96
-#define MMI_SOFT_REGS 200
+#define MMI_CTRL_REGS 88
+#define MMI_SOFT_REGS 208
 #endif
 constexpr int CTRL_REGS = MMI_CTRL_REGS;  // setmaxnreg budgets: .inc only draws on what .dec released
 constexpr int SOFT_REGS = MMI_SOFT_REGS;  // inside the CTA's launch allocation, else it blocks forever
@@ -623,6 +623,77 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             umma_commit(s_full + 2 * hf + 0);
             umma_commit(s_full + 2 * hf + 1);
           };
+#ifndef MMI_NO_STAGGER
+          // Staggered halves: the two softmax warpgroups share each sub-partition's MUFU, so the
+          // halves are kept half a period apart -- half B's first S is issued only after half A's
+          // first P V -- and the MMAs of one half are issued as a block (P V(t, 0), P V(t, 1),
+          // S(t + 1)): half A's tensor work then overlaps half B's softmax and vice versa, instead
+          // of both softmaxes convoying on the MUFU while the tensor pipe idles.
+          t0 = PROF_T();
+          mbar_wait(k_full + ks, k_phase);
+          PROF_ADD(wk, t0);
+          tc_fence_after();
+          uint32_t live_cur = (uint32_t)live_s[ks], live_next = 0;
+          int kcur = ks;  // K stage of tile 0, held until the last S of tile 0 is issued
+          if (++ks == KST) {
+            ks = 0;
+            k_phase ^= 1;
+          }
+          if (live_cur & 1u) issue_s128(0, kcur);
+          bool b_deferred = (nh > 1) && (live_cur & 2u);
+          if (!b_deferred) {
+            if (n == 1) umma_commit(q_empty);
+            umma_commit(k_empty + kcur);
+          }
+          for (int t = 0; t < n; ++t) {
+            const bool ahead = (t + 1 < n);
+            t0 = PROF_T();
+            mbar_wait(v_full + vs, v_phase);
+            PROF_ADD(wv, t0);
+            int knext = 0;
+            if (ahead) {
+              t0 = PROF_T();
+              mbar_wait(k_full + ks, k_phase);
+              PROF_ADD(wk, t0);
+              tc_fence_after();
+              live_next = (uint32_t)live_s[ks];
+              knext = ks;
+              if (++ks == KST) {
+                ks = 0;
+                k_phase ^= 1;
+              }
+            }
+#ifdef MMI_PROF
+            prof_nt += 2 * nh;
+#endif
+            if (live_cur & 1u) {
+              issue_pv(0, 2 * t);
+              issue_pv(0, 2 * t + 1);
+            }
+            if (ahead && (live_next & 1u)) issue_s128(0, knext);
+            if (b_deferred) {  // half B's first S, half a period behind half A
+              issue_s128(1, kcur);
+              b_deferred = false;
+              if (n == 1) umma_commit(q_empty);
+              umma_commit(k_empty + kcur);
+            }
+            if (nh > 1 && (live_cur & 2u)) {
+              issue_pv(1, 2 * t);
+              issue_pv(1, 2 * t + 1);
+            }
+            if (ahead) {
+              if (nh > 1 && (live_next & 2u)) issue_s128(1, knext);
+              if (t + 1 == n - 1) umma_commit(q_empty);  // last S of the item issued
+              umma_commit(k_empty + knext);
+            }
+            umma_commit(v_empty + vs);
+            if (++vs == VST) {
+              vs = 0;
+              v_phase ^= 1;
+            }
+            live_cur = live_next;
+          }
+#else
           t0 = PROF_T();
           mbar_wait(k_full + ks, k_phase);
           PROF_ADD(wk, t0);
@@ -672,6 +743,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             live_cur = live_next;
           }
+#endif
 #else
           // prologue: both sub-tiles of key tile 0 for every live half
           t0 = PROF_T();

@@ -140,3 +140,23 @@ def small_workload(S_frames: int = 8, text: int = 64, H: int = 2, Hkv: int = 1, 
 
 
 WORKLOADS = {i: (lambda i=i: build_workload(i)) for i in range(5)}
+
+
+# ---------------------------------------------------------------- extra (non-BASELINE) workloads
+def baselines_workload() -> Workload:
+    """f3 static baselines (tab:impl_details P:685-688) on the LongVILA-shaped 128K
+    layout: heads cycle A-shape(128, 4096), Tri-shape(128, 4096, 128), SparseTransformer fixed /
+    strided with Local = vline_stride = tokens per frame."""
+    from .config import trishape, sf_fixed, sf_strided
+    seg = _segments([("T", 64), ("F", 511), ("T", 192)])
+    pb = Problem(28, 4, sum(n for _, n in seg), 128, n_modalities=2)
+    cyc = [ashape(128, 4096), trishape(128, 4096, 128), sf_fixed(TPF, TPF), sf_strided(TPF, TPF)]
+    return Workload("baselines_128k", seg, pb, [HeadConfig.no_boundary(cyc[h % 4]) for h in range(28)])
+
+
+def natten_workload():
+    """f4 (App. F): a DiT-video-shaped layer -- 24 heads, D = 128, latent grid
+    16 x 48 x 80 (61,440 tokens), 3D neighborhood window 5 x 15 x 15, tiles 2 x 8 x 8."""
+    from .config import NattenConfig
+    nc = NattenConfig(16, 48, 80, 5, 15, 15, 2, 8, 8)
+    return "natten_dit_61k", Problem(24, 24, nc.seq_len, 128), nc
