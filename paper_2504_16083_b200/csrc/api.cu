@@ -275,7 +275,7 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
   // a3 grid stride / phase
   const DInst* dinsts = blob_at<DInst>(ws, P, P.o_insts);
   launch_grid(dinsts, blob_at<int>(ws, P, P.o_gi), P.n_grid, P.max_ncand, (int)P.insts.size(), dslabs, sinfo, info,
-              at<int>(ws, P.perm), at<float>(ws, P.cbuf), at<float>(ws, P.c_rank), S, P.S_pad,
+              at<int>(ws, P.perm), at<float>(ws, P.cbuf), at<uint32_t>(ws, P.c_rank), S, P.S_pad,
               at<GridRes>(ws, P.gridres), at<double>(ws, P.grid_part), blob_at<int64_t>(ws, P, P.o_gacc),
               at<uint32_t>(ws, P.grid_acc), s);
   // a4 vertical-slash top-k

@@ -623,8 +623,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             umma_commit(s_full + 2 * hf + 0);
             umma_commit(s_full + 2 * hf + 1);
           };
-#ifndef MMI_NO_STAGGER
-          // Staggered halves: the two softmax warpgroups share each sub-partition's MUFU, so the
+#ifdef MMI_STAGGER
+          // (experiment, off by default: measured 4 % slower at 128K and 1M) Staggered halves: the two softmax warpgroups share each sub-partition's MUFU, so the
           // halves are kept half a period apart -- half B's first S is issued only after half A's
           // first P V -- and the MMAs of one half are issued as a block (P V(t, 0), P V(t, 1),
           // S(t + 1)): half A's tensor work then overlaps half B's softmax and vice versa, instead

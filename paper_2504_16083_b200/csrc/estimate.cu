@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include "estimate.h"
+#include "ptx.cuh"
 
 namespace mmi {
 
@@ -512,18 +513,27 @@ cudaError_t launch_slabs(const DSlab* slabs, int n_slabs, int n_dg_batch, const 
 }
 
 // =============================================================== a3: grid
-// c_rank[g][rho] = c[P_a[rho]] for rank-coordinate grid instances
-__global__ void grid_gather_rank_kernel(const DInst* __restrict__ insts, int n_inst_total, const DSlab* __restrict__ slabs,
-                                        const int* __restrict__ info, const int* __restrict__ perm,
-                                        const float* __restrict__ cbuf, float* __restrict__ c_rank, int S_pad) {
+// fx[g][j] = round(c[j] * 2^25) in the pattern's coordinate system (rank-coordinate instances:
+// c[P_a[rho]]), for every estimated grid instance: the fold reads exact integers (see below)
+constexpr float FX25 = 33554432.0f;  // 2^25
+__global__ void grid_prep_kernel(const DInst* __restrict__ insts, int n_inst_total, const DSlab* __restrict__ slabs,
+                                 const int* __restrict__ info, const int* __restrict__ perm,
+                                 const float* __restrict__ cbuf, uint32_t* __restrict__ fx, int S, int S_pad) {
   const int ii = blockIdx.y;
   const DInst x = insts[ii];
-  if (x.kind != MMI_PAT_GRID || !x.rank || x.stat) return;
-  const int na = info[MI_CNT + x.qa];
-  const int off = info[MI_OFF + x.qa];
+  if (x.kind != MMI_PAT_GRID || x.stat) return;
   const DSlab sl = slabs[x.slab];
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < na; r += gridDim.x * blockDim.x)
-    c_rank[(size_t)x.grid_id * S_pad + r] = cbuf[sl.c_off + perm[off + r]];
+  const float* c = cbuf + sl.c_off;
+  uint32_t* out = fx + (size_t)x.grid_id * S_pad;
+  if (x.rank) {
+    const int na = info[MI_CNT + x.qa];
+    const int off = info[MI_OFF + x.qa];
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < na; r += gridDim.x * blockDim.x)
+      out[r] = __float2uint_rn(c[perm[off + r]] * FX25);
+  } else {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S; j += gridDim.x * blockDim.x)
+      out[j] = __float2uint_rn(c[j] * FX25);
+  }
 }
 
 struct JP {
@@ -548,14 +558,15 @@ __device__ __forceinline__ void grid_window(const DInst& x, const int* sinfo, co
 }
 
 // Fold (reading C4-C6): m_s[p] = sum_{j in W, j = p mod s} c[j] for every candidate stride.
-// c >= 0 is a column mass of at most L <= 64 softmax rows, so sum_j c[j] <= 64 and c can be taken
-// to 2^-25 fixed point (round to nearest) with every partial and total sum inside uint32: the
-// fold is exact integer arithmetic, hence order-independent and deterministic.
-// One CTA owns FOLD_SPC consecutive candidate strides and streams the whole window W through
-// shared memory (double-buffered cp.async chunks); thread (group g, phase p) of stride s <= 256
-// sums the chunk elements of absolute phase p at g*s + k*G*s (G = 256 / s groups), threads of
-// larger strides own up to FOLD_MAXW phases each.  Every stride's sums stay in registers across
-// chunks and are written once (no atomics).
+// c >= 0 is a column mass of at most L <= 64 softmax rows, so sum_j c[j] <= 64 and c is taken to
+// 2^-25 fixed point (round to nearest, grid_prep_kernel) with every partial and total sum inside
+// uint32: the fold is exact integer arithmetic, hence order-independent and deterministic.
+// One CTA owns FOLD_SPC consecutive strides s > smax / 2 (the others are derived exactly from a
+// multiple, grid_derive_kernel) and streams the window W through shared memory (double-buffered
+// bulk copies); thread (group g, phase p) of stride s <= 256 sums the chunk elements of phase p at
+// g*s + k*G*s (G = 256 / s groups), threads of larger strides own up to FOLD_MAXW phases each.
+// Every stride's sums stay in registers across chunks and are written once (no atomics); the chunk
+// phase offset advances incrementally (no divisions in the loop).
 #ifndef MMI_FOLD_CHUNK
 #define MMI_FOLD_CHUNK 8192
 #endif
@@ -563,34 +574,31 @@ constexpr int FOLD_CHUNK = MMI_FOLD_CHUNK;   // u32 keys per shared-memory chunk
 constexpr int FOLD_SPC = 8;                  // candidate strides per CTA
 constexpr int FOLD_THREADS = 256;
 constexpr int FOLD_MAXW = 4;                 // phases per thread for strides in (256, 1024]
-constexpr float FX25 = 33554432.0f;          // 2^25
 
-__device__ __forceinline__ void fold_load_chunk(uint32_t* dst, const float* __restrict__ c, int j0, int len) {
-  // fixed-point conversion happens at use; raw fp32 bits are staged with cp.async (16 B granules)
-  for (int i = threadIdx.x * 4; i < len; i += FOLD_THREADS * 4) {
-    const int j = j0 + i;
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + i);
-    if (i + 4 <= len && ((j & 3) == 0)) {
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(c + j) : "memory");
-    } else {
-      for (int e = 0; e < 4 && i + e < len; ++e) dst[i + e] = __float_as_uint(c[j + e]);
-    }
+// sum of ptr[0], ptr[step], ... below end (4 independent chains)
+__device__ __forceinline__ uint32_t strided_sum(const uint32_t* ptr, const uint32_t* end, int step) {
+  uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  const int s4 = 4 * step;
+  for (; ptr + 3 * step < end; ptr += s4) {
+    a0 += ptr[0];
+    a1 += ptr[step];
+    a2 += ptr[2 * step];
+    a3 += ptr[3 * step];
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (; ptr < end; ptr += step) a0 += *ptr;
+  return (a0 + a1) + (a2 + a3);
 }
 
 __global__ void __launch_bounds__(FOLD_THREADS) grid_acc_kernel(const DInst* __restrict__ insts,
                                                                 const int* __restrict__ grid_inst,
-                                                                const DSlab* __restrict__ slabs,
                                                                 const int* __restrict__ sinfo,
                                                                 const int* __restrict__ info,
-                                                                const float* __restrict__ cbuf,
-                                                                const float* __restrict__ c_rank, int S, int S_pad,
+                                                                const uint32_t* __restrict__ fx, int S, int S_pad,
                                                                 const int64_t* __restrict__ acc_off,
                                                                 uint32_t* __restrict__ acc) {
   extern __shared__ __align__(16) uint32_t fold_buf[];  // [2][FOLD_CHUNK]
-  uint32_t(*buf)[FOLD_CHUNK] = reinterpret_cast<uint32_t(*)[FOLD_CHUNK]>(fold_buf);
   __shared__ uint32_t part[FOLD_THREADS];
+  __shared__ __align__(8) uint64_t bar[2];
   const int gi = blockIdx.y;
   const DInst x = insts[grid_inst[gi]];
   if (x.stat) return;  // static grid: nothing to fold
@@ -602,67 +610,63 @@ __global__ void __launch_bounds__(FOLD_THREADS) grid_acc_kernel(const DInst* __r
   const int ns = min(FOLD_SPC, x.smax - s0 + 1);
   int lo, hi, n;
   grid_window(x, sinfo, info, S, lo, hi, n);
-  const float* c = x.rank ? c_rank + (size_t)gi * S_pad : cbuf + slabs[x.slab].c_off;
+  const uint32_t* c = fx + (size_t)gi * S_pad;
   const int tid = threadIdx.x;
   uint32_t accr[FOLD_SPC][FOLD_MAXW];
+  int rr[FOLD_SPC], cm[FOLD_SPC], pq[FOLD_SPC];
 #pragma unroll
-  for (int q = 0; q < FOLD_SPC; ++q)
+  for (int q = 0; q < FOLD_SPC; ++q) {
+    const int s = s0 + q;
 #pragma unroll
     for (int w = 0; w < FOLD_MAXW; ++w) accr[q][w] = 0u;
+    rr[q] = q < ns ? lo % s : 0;                     // phase of the chunk's first key
+    cm[q] = q < ns ? FOLD_CHUNK % s : 0;             // phase advance per chunk
+    pq[q] = q < ns && s <= FOLD_THREADS ? tid % s : 0;
+  }
+  // W is read with 16-byte bulk copies from a 16-byte aligned start (lo is a multiple of 128)
   const int nchunk = hi > lo ? (hi - lo + FOLD_CHUNK - 1) / FOLD_CHUNK : 0;
-  if (nchunk > 0) fold_load_chunk(buf[0], c, lo, min(FOLD_CHUNK, hi - lo));
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto load = [&](int ch) {
+    const int j0 = lo + ch * FOLD_CHUNK;
+    const int len = min(FOLD_CHUNK, hi - j0);
+    const uint32_t bytes = (uint32_t)((len + 3) & ~3) * 4u;  // reads <= 3 keys past hi, inside S_pad
+    mbar_arrive_expect_tx(&bar[ch & 1], bytes);
+    bulk_load(fold_buf + (ch & 1) * FOLD_CHUNK, c + j0, bytes, &bar[ch & 1]);
+  };
+  if (tid == 0 && nchunk > 0) load(0);
   for (int ch = 0; ch < nchunk; ++ch) {
-    const int j_begin = lo + ch * FOLD_CHUNK;
-    const int len = min(FOLD_CHUNK, hi - j_begin);
-    if (ch + 1 < nchunk) {
-      fold_load_chunk(buf[(ch + 1) & 1], c, j_begin + FOLD_CHUNK, min(FOLD_CHUNK, hi - j_begin - FOLD_CHUNK));
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    uint32_t* cb = buf[ch & 1];
-    // convert this chunk to fixed point in place (each element once)
-    for (int i = tid; i < len; i += FOLD_THREADS) cb[i] = __float2uint_rn(__uint_as_float(cb[i]) * FX25);
-    __syncthreads();
+    const int len = min(FOLD_CHUNK, hi - lo - ch * FOLD_CHUNK);
+    if (tid == 0 && ch + 1 < nchunk) load(ch + 1);  // buffer (ch+1)&1 was released by the last __syncthreads
+    mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
+    const uint32_t* cb = fold_buf + (ch & 1) * FOLD_CHUNK;
+    const uint32_t* end = cb + len;
 #pragma unroll
     for (int q = 0; q < FOLD_SPC; ++q) {
-      const int s = s0 + q;
       if (q >= ns) break;
-      const int r = j_begin % s;  // local index i has absolute phase (r + i) mod s
+      const int s = s0 + q, r = rr[q];
       if (s <= FOLD_THREADS) {
         const int G = FOLD_THREADS / s;
         if (tid < G * s) {
-          const int grp = tid / s, p = tid - grp * s;
-          const int i0 = (p >= r ? p - r : p - r + s) + grp * s;
-          const int step = G * s;
-          uint32_t a0 = 0, a1 = 0;
-          int i = i0;
-          for (; i + step < len; i += 2 * step) {
-            a0 += cb[i];
-            a1 += cb[i + step];
-          }
-          if (i < len) a0 += cb[i];
-          accr[q][0] += a0 + a1;
+          // tid = g * s + p: elements of phase p start at (p - r) mod s + g * s = tid - r (+ s)
+          const int i0 = tid - r + (pq[q] < r ? s : 0);
+          accr[q][0] += strided_sum(cb + i0, end, G * s);
         }
       } else {
 #pragma unroll
         for (int w = 0; w < FOLD_MAXW; ++w) {
           const int p = tid + w * FOLD_THREADS;
-          if (p < s) {
-            uint32_t a0 = 0, a1 = 0;
-            int i = p >= r ? p - r : p - r + s;
-            for (; i + s < len; i += 2 * s) {
-              a0 += cb[i];
-              a1 += cb[i + s];
-            }
-            if (i < len) a0 += cb[i];
-            accr[q][w] += a0 + a1;
-          }
+          if (p < s) accr[q][w] += strided_sum(cb + (p >= r ? p - r : p - r + s), end, s);
         }
       }
+      const int rn = r + cm[q];
+      rr[q] = rn >= s ? rn - s : rn;
     }
-    __syncthreads();  // buffer (ch & 1) is refilled two chunks later
+    __syncthreads();  // every thread is done with buffer ch & 1 before it is refilled
   }
   // combine the G groups of small strides; write m_s[p]
   uint32_t* g = acc + acc_off[gi];
@@ -825,16 +829,15 @@ __global__ void __launch_bounds__(1024) grid_pick_kernel(const DInst* __restrict
 
 void launch_grid(const DInst* insts, const int* grid_inst, int n_grid, int max_ncand, int n_inst_total,
                  const DSlab* slabs, const int* sinfo, const int* info, const int* perm, const float* cbuf,
-                 float* c_rank, int S, int S_pad, GridRes* res, double* part, const int64_t* acc_off,
+                 uint32_t* fx, int S, int S_pad, GridRes* res, double* part, const int64_t* acc_off,
                  uint32_t* acc, cudaStream_t st) {
   if (n_grid == 0) return;
-  grid_gather_rank_kernel<<<dim3(64, n_inst_total), 256, 0, st>>>(insts, n_inst_total, slabs, info, perm, cbuf,
-                                                                   c_rank, S_pad);
+  grid_prep_kernel<<<dim3(64, n_inst_total), 256, 0, st>>>(insts, n_inst_total, slabs, info, perm, cbuf, fx, S, S_pad);
   const int n_sg = (max_ncand + FOLD_SPC - 1) / FOLD_SPC;
   const int fold_smem = 2 * FOLD_CHUNK * (int)sizeof(uint32_t);
   cudaFuncSetAttribute(grid_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fold_smem);
-  grid_acc_kernel<<<dim3(n_sg, n_grid), FOLD_THREADS, fold_smem, st>>>(insts, grid_inst, slabs, sinfo, info, cbuf, c_rank, S,
-                                                                S_pad, acc_off, acc);
+  grid_acc_kernel<<<dim3(n_sg, n_grid), FOLD_THREADS, fold_smem, st>>>(insts, grid_inst, sinfo, info, fx, S, S_pad,
+                                                                       acc_off, acc);
   grid_derive_kernel<<<dim3(max_ncand, n_grid), 256, 0, st>>>(insts, grid_inst, acc_off, acc);
   grid_eval_kernel<<<dim3(max_ncand, n_grid), 256, 0, st>>>(insts, grid_inst, sinfo, info, S, acc_off, acc, part, res);
   grid_pick_kernel<<<n_grid, 1024, 0, st>>>(insts, grid_inst, part, res);

@@ -25,7 +25,7 @@ cudaError_t launch_slabs(const DSlab* slabs, int n_slabs, int n_dg_batch, const 
                          int ml_stride, cudaStream_t st);
 void launch_grid(const DInst* insts, const int* grid_inst, int n_grid, int max_ncand, int n_inst_total,
                  const DSlab* slabs, const int* sinfo, const int* info, const int* perm, const float* cbuf,
-                 float* c_rank, int S, int S_pad, GridRes* res, double* part, const int64_t* acc_off,
+                 uint32_t* fx, int S, int S_pad, GridRes* res, double* part, const int64_t* acc_off,
                  uint32_t* acc, cudaStream_t st);
 void launch_vs(const DInst* insts, const int* vs_inst, int n_vs, const DSlab* slabs, const int* sinfo, const int* info,
                const int* perm, const float* cbuf, const unsigned long long* dgbuf, const int64_t* list_off,

@@ -485,7 +485,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
   reg(P.slab_ml, sizeof(float) * 2 * ns * SLAB_ROWS);
   reg(P.cbuf, sizeof(float) * ns * nS);
   reg(P.dgbuf, sizeof(unsigned long long) * ns * nS);
-  reg(P.c_rank, sizeof(float) * std::max(P.n_grid, 1) * nS);
+  reg(P.c_rank, sizeof(uint32_t) * std::max(P.n_grid, 1) * nS);  // 2^-25 fixed-point c per grid instance
   reg(P.gridres, sizeof(GridRes) * std::max(P.n_grid, 1));
   reg(P.grid_part, sizeof(double) * 2 * std::max(P.n_grid, 1) * 1025);
   reg(P.grid_acc, sizeof(unsigned long long) * std::max<int64_t>(P.gacc_words, 1));

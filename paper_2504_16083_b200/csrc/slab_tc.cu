@@ -6,9 +6,10 @@
 // A-hat tile by tile and its column sums.  The slabs of one KV group are packed two per
 // tcgen05 M=128 tile (rows 0-63 slab a, 64-127 slab b); S = Q K^T (M128 N128) goes to a
 // double-buffered TMEM accumulator, K tiles arrive by TMA (128B swizzle) in a 2-stage ring,
-// and 4 epilogue warps (thread = TMEM lane = slab row) run the exp2 / statistics.  Column
-// sums over a warp's 32 rows use a butterfly transpose-reduce (31 shuffles per 32 columns),
-// the two warps of a slab are added in shared memory: fixed order, deterministic.
+// and 4 epilogue warps run the exp2 / statistics.  Pass 1 computes S = Q K^T (thread = TMEM lane
+// = slab row: row max / sum are per-thread); pass 2 computes S^T = K Q^T with the SAME shared
+// tiles as swapped operands (thread = key, columns = slab rows), so the column mass of a key is a
+// per-thread sum in fixed row order: no cross-thread reduction, deterministic.
 // Slabs that also need the diagonal mass dg (vertical-slash heads with slashes) run in
 // slab_kernel (estimate.cu), which accumulates both.
 #include <cuda.h>
@@ -149,8 +150,14 @@ __global__ void __launch_bounds__(STC_THREADS, 2)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k / 4) * (BLK * 128) + (k % 4) * 32;
-          umma_ss(tmem + b * 128, smem_desc(q_base + off, 16, 1024, 2),
-                  smem_desc(k_base + st * L::K_BYTES + off, 16, 1024, 2), IDESC, k > 0 ? 1u : 0u);
+          const uint64_t dq = smem_desc(q_base + off, 16, 1024, 2);
+          const uint64_t dk = smem_desc(k_base + st * L::K_BYTES + off, 16, 1024, 2);
+          // pass 1: S = Q K^T (TMEM lane = slab row); pass 2: S^T = K Q^T (TMEM lane = key), so the
+          // column sums of A-hat are per-thread sums over the TMEM columns
+          if (mode == 0)
+            umma_ss(tmem + b * 128, dq, dk, IDESC, k > 0 ? 1u : 0u);
+          else
+            umma_ss(tmem + b * 128, dk, dq, IDESC, k > 0 ? 1u : 0u);
         }
         umma_commit(k_empty + st);
         umma_commit(s_full + b);
@@ -159,27 +166,23 @@ __global__ void __launch_bounds__(STC_THREADS, 2)
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-    const bool valid = my_pos >= 0;
-    float m = -INFINITY, l = 0.f, inv_l = 0.f;
-    if (mode == 1 && valid) {
-      const float2 v = ml[(size_t)my_slab * SLAB_ROWS + rl];
-      m = v.x;
-      inv_l = v.y > 0.f ? 1.f / v.y : 0.f;
-    }
-    for (int i = 0; i < nt; ++i) {
-      const int b = i & 1;
-      const int j0 = (t_begin + i) * BLK;
-      mbar_wait(s_full + b, (i >> 1) & 1);
-      tc_fence_after();
-      // keys j0 + c admitted for this row iff j0 + c <= pos (causal; pos < S)
-      const int n_ok = valid ? min(max(my_pos - j0 + 1, 0), BLK) : 0;
+    if (mode == 0) {
+      // ---- pass 1: TMEM lane = slab row r; running max / normaliser over this chunk's keys ----
+      const bool valid = my_pos >= 0;
+      float m = -INFINITY, l = 0.f;
+      for (int i = 0; i < nt; ++i) {
+        const int b = i & 1;
+        const int j0 = (t_begin + i) * BLK;
+        mbar_wait(s_full + b, (i >> 1) & 1);
+        tc_fence_after();
+        // keys j0 + c admitted for this row iff j0 + c <= pos (causal; pos < S)
+        const int n_ok = valid ? min(max(my_pos - j0 + 1, 0), BLK) : 0;
 #pragma unroll
-      for (int c = 0; c < BLK / 32; ++c) {
-        uint32_t raw[32];
-        tmem_ld32(tmem + b * 128 + c * 32 + lane_off, raw);
-        tmem_wait_ld();
-        float v[32];
-        if (mode == 0) {
+        for (int c = 0; c < BLK / 32; ++c) {
+          uint32_t raw[32];
+          tmem_ld32(tmem + b * 128 + c * 32 + lane_off, raw);
+          tmem_wait_ld();
+          float v[32];
           float mx = -INFINITY;
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
@@ -194,30 +197,89 @@ __global__ void __launch_bounds__(STC_THREADS, 2)
             l = (m > -INFINITY ? l * ex2(m - mn) : 0.f) + sum;
             m = mn;
           }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 32; ++k)
-            v[k] = (c * 32 + k < n_ok) ? ex2(__uint_as_float(raw[k]) * scale_log2 - m) * inv_l : 0.f;
-          const float colsum = warp_colsum32(v, lane);  // column c*32 + lane over this warp's 32 rows
-          cs[ew * BLK + c * 32 + lane] = colsum;
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty + b);  // S buffer b may be overwritten
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_empty + b);  // S buffer b may be overwritten
-      if (mode == 1) {
-        named_bar_sync(1, 128);
-        // thread t (0..127) owns key column t: slab a = warps 0+1, slab b = warps 2+3
-        const int t = ew * 32 + lane, j = j0 + t;
-        if (j < S) {
-          cbuf[SA.c_off + j] = cs[t] + cs[BLK + t];
-          if (sb >= 0) cbuf[slabs[sb].c_off + j] = cs[2 * BLK + t] + cs[3 * BLK + t];
+      if (my_slab >= 0) ml_part[((size_t)my_slab * ml_stride + chunk) * SLAB_ROWS + rl] = make_float2(m, l);
+    } else {
+      // ---- pass 2: TMEM lane = key j, column = slab row r; c[j] = sum_r A-hat[r, j] per thread ----
+      // A-hat[r, j] = exp2(z * scale - Mr), Mr = m_r + log2(l_r) (+inf for rows without keys); row r
+      // admits key j iff pos_r >= j: slab rows are ascending, so that is a suffix of each slab's rows
+      float* Mr = cs;                                       // [128]
+      int* pos_s = reinterpret_cast<int*>(cs + BLK);        // [128] (-1: no row)
+      {
+        const int t = threadIdx.x - 128;  // 0..127: row t of the packed tile
+        const int sl = t < 64 ? sa : sb;
+        int pos = -1;
+        float M = INFINITY;
+        if (sl >= 0) {
+          pos = rows[sl * SLAB_ROWS + (t & 63)];
+          if (pos >= 0) {
+            const float2 v = ml[(size_t)sl * SLAB_ROWS + (t & 63)];
+            if (v.y > 0.f) M = v.x + __log2f(v.y);
+          }
         }
+        Mr[t] = M;
+        pos_s[t] = pos;
         named_bar_sync(1, 128);
+      }
+      const int La = sinfo[sa * 4 + 0], Lb = sb >= 0 ? sinfo[sb * 4 + 0] : 0;
+      const int key = ew * 32 + lane;  // TMEM lane
+      for (int i = 0; i < nt; ++i) {
+        const int b = i & 1;
+        const int j = (t_begin + i) * BLK + key;
+        // first row of each slab whose position is >= j (binary search over the ascending rows)
+        int lo_a = 0, hi_a = La;
+        while (lo_a < hi_a) {
+          const int mid = (lo_a + hi_a) >> 1;
+          if (pos_s[mid] >= j) hi_a = mid; else lo_a = mid + 1;
+        }
+        int lo_b = 0, hi_b = Lb;
+        while (lo_b < hi_b) {
+          const int mid = (lo_b + hi_b) >> 1;
+          if (pos_s[64 + mid] >= j) hi_b = mid; else lo_b = mid + 1;
+        }
+        mbar_wait(s_full + b, (i >> 1) & 1);
+        tc_fence_after();
+        float ca = 0.f, cbs = 0.f;
+#pragma unroll
+        for (int c = 0; c < BLK / 32; ++c) {
+          // admitted rows of this 32-row chunk as a bit mask: [lo, L) of its slab, chunk-local
+          const int base = (c & 1) * 32;
+          const int lo = (c < 2 ? lo_a : lo_b) - base, hi = (c < 2 ? La : Lb) - base;
+          const int l0 = min(max(lo, 0), 32), h0 = min(max(hi, 0), 32);
+          const uint32_t mask = (h0 > l0) ? ((h0 == 32 ? 0xffffffffu : ((1u << h0) - 1u)) & ~((1u << l0) - 1u)) : 0u;
+          if (!__any_sync(0xffffffffu, mask != 0u)) continue;  // no admitted row in this chunk for the warp
+          uint32_t raw[32];
+          tmem_ld32(tmem + b * 128 + c * 32 + lane_off, raw);
+          tmem_wait_ld();
+          float acc = 0.f;
+#pragma unroll
+          for (int k4 = 0; k4 < 32; k4 += 4) {
+            const float4 M4 = *reinterpret_cast<const float4*>(Mr + c * 32 + k4);
+            const float Mk[4] = {M4.x, M4.y, M4.z, M4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float v = ex2(__uint_as_float(raw[k4 + e]) * scale_log2 - Mk[e]);
+              acc += ((mask >> (k4 + e)) & 1u) ? v : 0.f;
+            }
+          }
+          if (c < 2)
+            ca += acc;
+          else
+            cbs += acc;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty + b);
+        if (j < S) {
+          cbuf[SA.c_off + j] = ca;
+          if (sb >= 0) cbuf[slabs[sb].c_off + j] = cbs;
+        }
       }
     }
-    if (mode == 0 && my_slab >= 0)
-      ml_part[((size_t)my_slab * ml_stride + chunk) * SLAB_ROWS + rl] = make_float2(m, l);
   }
   tc_fence_before();
   __syncthreads();
