@@ -18,7 +18,6 @@
 
 namespace mmi {
 
-constexpr int LONG_ITEM_TILES = 48;
 
 __device__ __forceinline__ int pad128d(int x) { return (x + BLK - 1) / BLK * BLK; }
 __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
@@ -517,7 +516,17 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
 }
 
 // builds (or counts) one work-item slot
-__device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W) {
+// Work order (ascending 32-bit key, stable): the L2 reuse of key tiles decides the kernel's DRAM
+// traffic at 1M tokens, so items that read the same keys run at the same time:
+//   class 0  very long items (>= LONG_LIVE live tile-halves), longest first (load balance);
+//   class 1  h-row split-K chunks by (key chunk, KV group, row pair, head): every pair and every
+//            h-line head of a group reads the same 65536 keys of a chunk;
+//   class 2  MAIN items by (row position, head): the heads of a KV group share the band / sink tiles;
+//   class 3  SLASH items by (head, residue class, pair): the pairs of a class share its K̄ tiles.
+constexpr int LONG_LIVE = 4096;
+__device__ __forceinline__ uint32_t order_key(uint32_t cls, uint32_t v) { return (cls << 30) | (v & 0x3FFFFFFFu); }
+
+__device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W, uint32_t& okey) {
   // locate the pass
   int lo = 0, hi = C.n_passes - 1;
   while (lo < hi) {
@@ -615,6 +624,7 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
       W.out_row0 = hd.part_rows0 + row_in_view;
     }
     W.pad[0] = R.xp_lo;
+    okey = order_key(2, (uint32_t)(R.xp_lo / BLK) * 64u + (uint32_t)(I.h & 63));
     for (int ii = 0; ii < hd.n_inst; ++ii) {
       const DInst x = C.insts[I.h * MAX_INST + ii];
       if (x.qa >= 0 && x.qa != grp) continue;
@@ -638,6 +648,8 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
       W.q_row0 = qv.row_off + t0;
       W.out_mode = OUT_PARTIAL;
       W.out_row0 = x.pad[1] + chunk * qv.cap + t0;
+      okey = order_key(1, ((uint32_t)min(chunk, 127) << 23) | ((uint32_t)(I.kv & 31) << 18) |
+                              ((uint32_t)min(b / n_split, 4095) << 6) | (uint32_t)(I.h & 63));
     } else {
       // pair b inside residue class r: classes r < rem hold q+1 keys, the others q
       ClassGeo cg;
@@ -656,6 +668,7 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W)
       if (r == g.p && (x.flags & (GF_H | GF_V))) return;  // class p owned by H / V passes (C9)
       nr = cg.nr(r);
       t0 = 2 * kk * BLK;
+      okey = order_key(3, ((uint32_t)(I.h & 63) << 22) | ((uint32_t)min(r, 1023) << 12) | (uint32_t)min(kk, 4095));
       const int res_row = cg.classoff(r) + t0;
       const DView qv = C.views[x.v_res_q];
       W.q_row0 = qv.row_off + res_row;
@@ -732,7 +745,8 @@ __global__ void items_count_kernel(IndexCtx C) {
   E.out = nullptr;
   E.n_segs = E.n_tiles = E.n_live = 0;
   WorkItem W;
-  build_slot(C, slot, E, W);
+  uint32_t okey = 0;
+  build_slot(C, slot, E, W, okey);
   C.seg_cnt[slot] = E.n_segs;
 }
 
@@ -748,31 +762,38 @@ __global__ void items_fill_kernel(IndexCtx C) {
     // (its rows are not computed) and mmi_workspace_flags reports it
     atomicOr(C.flags, FLAG_SEG_OVERFLOW);
     E.out = nullptr;
-    build_slot(C, slot, E, W);
+    uint32_t okey = 0;
+    build_slot(C, slot, E, W, okey);
     W.seg_off = off;
     W.n_segs = W.n_tiles = 0;
     W.pad[1] = 0;
     C.items[slot] = W;
-    C.sort_keys[slot] = ~0;
+    C.sort_keys[slot] = (int)0xFFFFFFFFu;
     C.sort_vals[slot] = slot;
     return;
   }
   E.out = C.segs + off;
-  build_slot(C, slot, E, W);
+  uint32_t okey = 0;
+  build_slot(C, slot, E, W, okey);
   W.seg_off = off;
   W.n_segs = E.n_segs;
   W.n_tiles = E.n_tiles;
   W.pad[1] = E.n_live;
   C.items[slot] = W;
-  // work order: long items first by length (LPT); short items by position then head,
-  // so that concurrently running CTAs share the key tiles of a KV group in L2.
-  // (sorted ascending on the bitwise complement: descending key, equal keys keep slot order)
-  int key = 0;
-  if (E.n_live >= 2 * LONG_ITEM_TILES)
-    key = 0x40000000 + E.n_live;
+  // work order (see order_key); empty items last (the kernel stops at the first one)
+  uint32_t key = 0xFFFFFFFFu;
+#ifdef MMI_ORDER_LPT  // round-1 order (A/B experiments): long items by length, others by position
+  if (E.n_live >= 96)
+    key = ~(uint32_t)(0x40000000 + E.n_live);
   else if (E.n_tiles > 0)
-    key = 0x3FFFFFFF - ((W.pad[0] / BLK) * 64 + (W.head & 63));
-  C.sort_keys[slot] = ~key;
+    key = ~(uint32_t)(0x3FFFFFFF - ((W.pad[0] / BLK) * 64 + (W.head & 63)));
+#else
+  if (E.n_live >= LONG_LIVE)
+    key = order_key(0, 0x3FFFFFFFu - (uint32_t)E.n_live);
+  else if (E.n_tiles > 0)
+    key = okey;
+#endif
+  C.sort_keys[slot] = (int)key;
   C.sort_vals[slot] = slot;
 }
 
