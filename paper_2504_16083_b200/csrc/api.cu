@@ -184,6 +184,7 @@ static IndexCtx make_ctx(const Plan& P, void* ws) {
   C.vs_list_off = blob_at<int64_t>(ws, P, P.o_vsl);
   C.vs_bits_off = blob_at<int64_t>(ws, P, P.o_vsb);
   C.view_len = at<int>(ws, P.view_len);
+  C.view_alias = at<int>(ws, P.view_alias);
   C.qg_pos = at<int>(ws, P.qg_pos);
   C.qg_rank = at<int>(ws, P.qg_rank);
   C.qg_src = at<int>(ws, P.qg_src);

@@ -77,6 +77,41 @@ __device__ __forceinline__ int upper_bound_i(const int* a, int n, int v) {
   return lo;
 }
 
+// ================================================================ K-view dedupe
+// The gathered K̄ / V̄ view of a pattern depends only on (KV group, view kind, classes, modality,
+// stride, phase) -- not on the query head -- so the heads of a KV group whose estimated grids agree
+// share one copy (SURVEY §7 hard part (g)): alias[v] = the first K-space view with the same key.
+// Modality views (2D heads) of a group are identical; VS column views stay per head.
+__global__ void view_alias_kernel(IndexCtx C, int n_views) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n_views) return;
+  const DView a = C.views[v];
+  int canon = v;
+  if (a.space == 1 && a.kind != VK_VCOL) {
+    const int kva = C.heads[a.head].kv;
+    int sa = 0, pa = 0;
+    if (a.kind == VK_ORIG_CLASS || a.kind == VK_RANK_CLASS) {
+      const GridRes g = C.gridres[C.insts[a.head * MAX_INST + a.inst].grid_id];
+      sa = g.s;
+      pa = a.classes ? g.p : 0;
+    }
+    for (int u = 0; u < v; ++u) {
+      const DView b = C.views[u];
+      if (b.space != 1 || b.kind != a.kind || b.classes != a.classes || b.mod != a.mod) continue;
+      if (C.heads[b.head].kv != kva) continue;
+      if (a.kind == VK_ORIG_CLASS || a.kind == VK_RANK_CLASS) {
+        const GridRes g = C.gridres[C.insts[b.head * MAX_INST + b.inst].grid_id];
+        if (g.s != sa || (a.classes ? g.p : 0) != pa) continue;
+      }
+      canon = u;
+      break;
+    }
+  }
+  C.view_alias[v] = canon;
+}
+
+__device__ __forceinline__ int kview_row0(const IndexCtx& C, int v) { return C.views[C.view_alias[v]].row_off; }
+
 // ================================================================ views
 __global__ void build_views_kernel(IndexCtx C, int space, const int* __restrict__ view_ids, int n_view_ids,
                                    int64_t rows_total) {
@@ -104,6 +139,13 @@ __global__ void build_views_kernel(IndexCtx C, int space, const int* __restrict_
     pos_a[row] = PADPOS;
     rank_a[row] = PADPOS;
     src_a[row] = -2;
+    return;
+  }
+  if (space && C.view_alias[v] != v) {  // deduplicated K view: its canonical copy is gathered instead
+    pos_a[row] = PADPOS;
+    rank_a[row] = PADPOS;
+    src_a[row] = -2;
+    if (row == C.views[v].row_off) C.view_len[v] = 0;
     return;
   }
   const DView dv = C.views[v];
@@ -400,7 +442,7 @@ __device__ KView base_kview(const IndexCtx& C, const ItemCtx& I, const DInst& x)
     const int b = x.kb;
     k.kind = 1;
     k.space = 1;
-    k.row0 = C.views[I.hd->kmod_view].row_off + C.info[MI_PADOFF + b];
+    k.row0 = kview_row0(C, I.hd->kmod_view) + C.info[MI_PADOFF + b];
     k.n = C.info[MI_CNT + b];
     k.kv_base = 0;
     k.pos_of_rank = C.perm + C.info[MI_OFF + b];
@@ -449,11 +491,10 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
     }
     if (x.kind == MMI_PAT_GRID && (x.flags & GF_V)) {
       const GridRes g = C.gridres[x.grid_id];
-      const DView cv = C.views[x.v_cls_k];
       KView kc;
       kc.kind = 2;
       kc.space = 1;
-      kc.row0 = cv.row_off;
+      kc.row0 = kview_row0(C, x.v_cls_k);
       const int n = rmode ? C.info[MI_CNT + x.qa] : C.S;
       kc.n = g.p < n ? (n - g.p + g.s - 1) / g.s : 0;
       kc.cls_r = g.p;
@@ -718,13 +759,12 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W,
       }
     } else {
       // same residue class of the key base, causal, minus the A-part (role NOTA)
-      const DView kvw = C.views[x.v_res_k];
       ClassGeo cg;
       cg.init(n, g.s);
       KView kc;
       kc.kind = 2;
       kc.space = 1;
-      kc.row0 = kvw.row_off + cg.classoff(r);
+      kc.row0 = kview_row0(C, x.v_res_k) + cg.classoff(r);
       kc.n = nr;
       kc.cls_r = r;
       kc.cls_s = g.s;
@@ -998,6 +1038,8 @@ void launch_hrow_merge(const IndexCtx& C, int D, const DHrow* hrows, int n_hrows
 }
 void launch_build_views(const IndexCtx& C, const int* qviews, int nq, const int* kviews, int nk, int64_t qrows,
                         int64_t krows, cudaStream_t st) {
+  const int nv = nq + nk;
+  if (nv > 0) view_alias_kernel<<<(nv + 127) / 128, 128, 0, st>>>(C, nv);
   if (qrows > 0) build_views_kernel<<<(unsigned)((qrows + 255) / 256), 256, 0, st>>>(C, 0, qviews, nq, qrows);
   if (krows > 0) build_views_kernel<<<(unsigned)((krows + 255) / 256), 256, 0, st>>>(C, 1, kviews, nk, krows);
 }

@@ -25,6 +25,7 @@ struct IndexCtx {
   const int64_t* vs_list_off;
   const int64_t* vs_bits_off;
   int* view_len;
+  int* view_alias;      // K-view dedupe: canonical view of each view
   int *qg_pos, *qg_rank, *qg_src, *kg_pos, *kg_rank, *kg_src;
   InstParam* inst_params;
   int* seg_cnt;

@@ -493,6 +493,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
   reg(P.vs_cnt, sizeof(int) * 2 * std::max(P.n_vs, 1));
   reg(P.bits, sizeof(uint32_t) * std::max<int64_t>(P.bits_words, 1));
   reg(P.view_len, sizeof(int) * std::max<size_t>(P.views.size(), 1));
+  reg(P.view_alias, sizeof(int) * std::max<size_t>(P.views.size(), 1));
   reg(P.qg_pos, sizeof(int) * P.qg_rows);
   reg(P.qg_rank, sizeof(int) * P.qg_rows);
   reg(P.qg_src, sizeof(int) * P.qg_rows);

@@ -124,7 +124,7 @@ struct Plan {
   Region labels, mod_cnt, mod_off, perm, rank, modpos, modrank;
   Region slab_rows, slab_ml_part, slab_ml, cbuf, dgbuf, c_rank;
   Region gridres, grid_part, grid_acc, vs_lists, vs_cnt, bits;
-  Region view_len;
+  Region view_len, view_alias;
   Region qg_pos, qg_rank, qg_src, kg_pos, kg_rank, kg_src, qg, kg, vg;
   Region items, item_keys, item_vals, items_sorted, seg_cnt, seg_off, segs, inst_params, sort_tmp, scan_tmp;
   Region part_o, part_lse;
