@@ -59,12 +59,22 @@ constexpr int SCHED_RING = 4;
 constexpr int SCHED_ENTRY = 128;  // bytes per ring entry: item index + staged WorkItem
 static_assert(16 + sizeof(WorkItem) <= SCHED_ENTRY, "WorkItem does not fit the scheduler ring entry");
 constexpr int NWARP_CTRL = 4;                      // scheduler+Q, MMA, K loader, V loader
-constexpr int NWARP_SOFT = 8;                      // 2 softmax warpgroups: one per query half
+#ifndef MMI_HPW
+#define MMI_HPW 1
+#endif
+constexpr int HPW = MMI_HPW;                       // query halves per softmax warpgroup (1 or 2)
+static_assert(HPW == 1 || HPW == 2, "HPW must be 1 or 2");
+constexpr int NWARP_SOFT = 8 / HPW;                // softmax warpgroups: one per half, or one for both
 constexpr int NTHREADS = 32 * (NWARP_CTRL + NWARP_SOFT);
-constexpr int LAUNCH_REGS = 168;                   // ptxas allocation at __launch_bounds__(384, 1)
+constexpr int LAUNCH_REGS = (HPW == 1) ? 168 : 255;  // ptxas allocation at __launch_bounds__(NTHREADS, 1)
 #ifndef MMI_CTRL_REGS
+#if MMI_HPW == 1
 #define MMI_CTRL_REGS 88
 #define MMI_SOFT_REGS 208
+#else
+#define MMI_CTRL_REGS 0  // 256 threads: every warp keeps the launch allocation
+#define MMI_SOFT_REGS 0
+#endif
 #endif
 constexpr int CTRL_REGS = MMI_CTRL_REGS;  // setmaxnreg budgets: .inc only draws on what .dec released
 constexpr int SOFT_REGS = MMI_SOFT_REGS;  // inside the CTA's launch allocation, else it blocks forever
@@ -89,6 +99,20 @@ __device__ unsigned long long g_prof[32];
 #define PROF_ADD(n, t0)
 #define PROF_FLUSH(i, n)
 #endif
+// MMI_TRACE builds (scratch only): per-event SM clock stamps of CTA 0 -- region 0 the MMA issuer,
+// 1 / 2 lane 0 of the first softmax warp of half A / B; event = (clock - t0) << 8 | code << 4 | arg
+#ifdef MMI_TRACE
+constexpr int TRACE_N = 16384;
+__device__ unsigned long long g_trace[3][TRACE_N];
+__device__ int g_trace_n[3];
+#define TRACE(reg, code, arg)                                                                          \
+  do {                                                                                                 \
+    if (blockIdx.x == 0 && tr_n < TRACE_N)                                                             \
+      g_trace[reg][tr_n++] = ((unsigned long long)(clock64() - tr_t0) << 8) | ((code) << 4) | (arg);   \
+  } while (0)
+#else
+#define TRACE(reg, code, arg)
+#endif
 
 template <int D>
 struct Smem {
@@ -106,8 +130,8 @@ struct Smem {
   static constexpr int OFF_EPI = (OFF_RI + 2 * 2 * 2 * BLK * 4 + 1023) & ~1023;
   static constexpr int OFF_BAR = OFF_EPI + NWARP_SOFT * 32 * EPI_STRIDE;
   // q_full q_empty k_full[KST] k_empty[KST] v_full[VST] v_empty[VST] s_full[2][2] p_full[2][2] o_full[2]
-  // o_empty[2] pv_done[2] sched_full[R] sched_empty[R] kp_full[NKP] kp_empty[NKP]
-  static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 14 + 2 * SCHED_RING + 2 * NKP + 4;
+  // o_empty[2] pv_done[2][2] sched_full[R] sched_empty[R] kp_full[NKP] kp_empty[NKP]
+  static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + 16 + 2 * SCHED_RING + 2 * NKP + 4;
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
   static constexpr int OFF_LIVE = OFF_TMEM + 16;  // [KST] live-half bits of the tile in each K stage
   static constexpr int TOTAL = OFF_LIVE + 16;
@@ -329,8 +353,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* p_full = s_full + 4;     // [half][slot]: P (bf16, aliasing S in TMEM) written by the softmax
   uint64_t* o_full = p_full + 4;     // [half]
   uint64_t* o_empty = o_full + 2;    // [half]
-  uint64_t* pv_done = o_empty + 2;   // [half]: one commit per P V
-  uint64_t* sched_full = pv_done + 2;
+  uint64_t* pv_done = o_empty + 2;   // [half][slot]: one commit per P V
+  uint64_t* sched_full = pv_done + 4;
   uint64_t* sched_empty = sched_full + SCHED_RING;
   uint64_t* kp_full = sched_empty + SCHED_RING;
   uint64_t* ri_full = kp_full + 2 * NKP;  // [2] row identities (positions / ranks) of an item staged
@@ -364,7 +388,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(o_full + i, 1);
       mbar_init(o_empty + i, 128);
-      mbar_init(pv_done + i, 1);
+      mbar_init(pv_done + 2 * i, 1);
+      mbar_init(pv_done + 2 * i + 1, 1);
     }
     for (int i = 0; i < SCHED_RING; ++i) {
       mbar_init(sched_full + i, 1);
@@ -393,6 +418,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+#ifdef MMI_TRACE
+  const long long tr_t0 = clock64();
+  int tr_n = 0;
+  const int tr_reg = (warp == 1) ? 0 : (warp == NWARP_CTRL && lane == 0) ? 1 : (warp == NWARP_CTRL + 4 && lane == 0) ? 2 : -1;
+#define TR(code, arg) do { if (tr_reg >= 0) TRACE(tr_reg, code, arg); } while (0)
+#else
+#define TR(code, arg)
+#endif
   // TMEM columns: S/P of half h at 128 h, O of half h at 256 + 128 h
   const int n_items = P.dense ? P.H * ((((P.S + BLK - 1) / BLK) + 1) / 2) : P.n_items;
   auto fetch = [&](int i) -> int {
@@ -406,7 +439,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   };
 
   if (warp < NWARP_CTRL) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(CTRL_REGS));
+    if (CTRL_REGS > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(CTRL_REGS > 0 ? CTRL_REGS : 256));
     if (warp == 0) {
       // ======================= scheduler + Q loader =======================
       // lane 0 schedules and stages; the whole warp issues the row gathers of permuted Q blocks
@@ -539,17 +572,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     } else {
       // ======================= MMA issuer (one thread) =======================
-      // Sub-tile j = 2t + u covers keys [64u, 64u + 64) of key tile t.  S_h(j) goes to slot u
-      // (TMEM columns [64u, 64u + 64) of half h's S buffer) and P_h(j) overwrites its first 32
-      // columns, so S_h(j + 1) (other slot) is issued before P_h(j) V: the softmax of a half
-      // always finds its next scores ready and runs back to back.
+      // Per key tile t: P_A(t, 0) V, P_B(t, 0) V, P_A(t, 1) V, S_A(t + 1), P_B(t, 1) V, S_B(t + 1),
+      // where sub-tile (t, u) = keys [64u, 64u + 64) of the tile, S_h(t) is one M128 N128 group
+      // into both 64-column slots of half h's S buffer and P_h(t, u) overwrites the first 32 columns
+      // of slot u.  (Measured alternatives, tests/issuer_sim.py: a dynamic issuer advancing each
+      // half independently with N=64 scores one tile ahead was 1.6x slower -- with 2-stage K/V
+      // rings the halves drift apart and stall on each other's stage releases.)
       if (elect_one()) {
-        constexpr uint32_t IDESC_S = idesc_bf16(128, 64, 0);
         constexpr uint32_t IDESC_S128 = idesc_bf16(128, 128, 0);
         constexpr uint32_t IDESC_O = idesc_bf16(128, D, 1);
         const uint32_t q_base = smem_u32(smem + L::OFF_Q);
         const uint32_t k_base = smem_u32(smem + L::OFF_K);
         const uint32_t v_base = smem_u32(smem + L::OFF_V);
+        // operand descriptors: base descriptor + (byte offset >> 4) in the start-address field
+        const uint64_t dq0 = smem_desc(q_base, 16, 1024, 2), dk0 = smem_desc(k_base, 16, 1024, 2);
+        const uint64_t dv0 = smem_desc(v_base, BLK * 128, 1024, 2);
         int ks = 0, vs = 0;
         uint32_t k_phase = 0, v_phase = 0, q_phase = 0;
         uint32_t p_bits = 0, o_bits = 0;  // phase bits: P per (half, slot), O per half (no indexed arrays: they would live in local memory)
@@ -563,24 +600,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int n = it.n_tiles;
           if (n <= 0) continue;
           const int nh = it.has_b ? 2 : 1;
-          const int nsub = 2 * n;
           long long t0 = PROF_T();
           mbar_wait(q_full, q_phase);
           PROF_ADD(wq, t0);
+          TR(3, 0);
           q_phase ^= 1;
           tc_fence_after();
-          // S_h(j) = Q_h K(j)^T, 64 keys, K stage kst
-          auto issue_s = [&](int hf, int j, int kst) {
-            const int u = j & 1;
-#pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const uint32_t off = (k / 4) * (BLK * 128) + (k % 4) * 32;
-              const uint64_t ad = smem_desc(q_base + hf * L::Q_BYTES + off, 16, 1024, 2);
-              const uint64_t bd = smem_desc(k_base + kst * L::KV_BYTES + u * 64 * 128 + off, 16, 1024, 2);
-              umma_ss(tmem + 128 * hf + 64 * u, ad, bd, IDESC_S, k > 0 ? 1u : 0u);
-            }
-            umma_commit(s_full + 2 * hf + u);
-          };
           // O_h += P_h(j) V(j), P read from TMEM (A operand), V stage vs; `started` bit hf: O_h
           // already holds a P V of this item
           uint32_t started = 0;
@@ -595,105 +620,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (first) mbar_wait(o_empty + hf, ((o_bits >> hf) & 1u) ^ 1u);  // previous item's epilogue read O_h
             PROF_ADD(wo, t0);
             tc_fence_after();
+            TR(1, 2 * hf + u);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const uint64_t bd = smem_desc(v_base + vs * L::KV_BYTES + (4 * u + k) * 2048, BLK * 128, 1024, 2);
+              const uint64_t bd = dv0 + (uint64_t)((vs * L::KV_BYTES + (4 * u + k) * 2048) >> 4);
               umma_ts(tmem + 256 + 128 * hf, tmem + 128 * hf + 64 * u + k * 8, bd, IDESC_O,
                       (!first || k > 0) ? 1u : 0u);
             }
             started |= 1u << hf;
-            umma_commit(pv_done + hf);  // lets the softmax rescale O_h once this P V has landed
+            umma_commit(pv_done + 2 * hf + u);  // one phase per P V (slot u), consumed by the softmax
           };
           // Tiles dead for a half (no admitted element for its rows, per the index's per-half tile
           // states) issue neither its S nor its P V; the K loader passes each stage's live-half bits.
-#ifndef MMI_S64
           // S of a whole 128-key tile is ONE M128 N128 MMA group into both 64-column slots of the
           // half (full tensor rate: A 4 KB + B 4 KB of shared memory per 64 clk; two N=64 groups
           // cost 2 x 48 clk, bound by the 128 B/clk operand bandwidth).  S_h(t+1) overwrites P_h(t),
           // so it is issued right after P_h(t, u=1) V: the other half's work fills the MMA pipe while
           // this half's softmax runs.
           auto issue_s128 = [&](int hf, int kst) {
+            TR(2, 2 * hf);
 #pragma unroll
             for (int k = 0; k < D / 16; ++k) {
               const uint32_t off = (k / 4) * (BLK * 128) + (k % 4) * 32;
-              const uint64_t ad = smem_desc(q_base + hf * L::Q_BYTES + off, 16, 1024, 2);
-              const uint64_t bd = smem_desc(k_base + kst * L::KV_BYTES + off, 16, 1024, 2);
+              const uint64_t ad = dq0 + (uint64_t)((hf * L::Q_BYTES + off) >> 4);
+              const uint64_t bd = dk0 + (uint64_t)((kst * L::KV_BYTES + off) >> 4);
               umma_ss(tmem + 128 * hf, ad, bd, IDESC_S128, k > 0 ? 1u : 0u);
             }
-            umma_commit(s_full + 2 * hf + 0);
-            umma_commit(s_full + 2 * hf + 1);
+            umma_commit(s_full + 2 * hf);  // both 64-key slots: one phase per tile
           };
-#ifdef MMI_STAGGER
-          // (experiment, off by default: measured 4 % slower at 128K and 1M) Staggered halves: the two softmax warpgroups share each sub-partition's MUFU, so the
-          // halves are kept half a period apart -- half B's first S is issued only after half A's
-          // first P V -- and the MMAs of one half are issued as a block (P V(t, 0), P V(t, 1),
-          // S(t + 1)): half A's tensor work then overlaps half B's softmax and vice versa, instead
-          // of both softmaxes convoying on the MUFU while the tensor pipe idles.
-          t0 = PROF_T();
-          mbar_wait(k_full + ks, k_phase);
-          PROF_ADD(wk, t0);
-          tc_fence_after();
-          uint32_t live_cur = (uint32_t)live_s[ks], live_next = 0;
-          int kcur = ks;  // K stage of tile 0, held until the last S of tile 0 is issued
-          if (++ks == KST) {
-            ks = 0;
-            k_phase ^= 1;
-          }
-          if (live_cur & 1u) issue_s128(0, kcur);
-          bool b_deferred = (nh > 1) && (live_cur & 2u);
-          if (!b_deferred) {
-            if (n == 1) umma_commit(q_empty);
-            umma_commit(k_empty + kcur);
-          }
-          for (int t = 0; t < n; ++t) {
-            const bool ahead = (t + 1 < n);
-            t0 = PROF_T();
-            mbar_wait(v_full + vs, v_phase);
-            PROF_ADD(wv, t0);
-            int knext = 0;
-            if (ahead) {
-              t0 = PROF_T();
-              mbar_wait(k_full + ks, k_phase);
-              PROF_ADD(wk, t0);
-              tc_fence_after();
-              live_next = (uint32_t)live_s[ks];
-              knext = ks;
-              if (++ks == KST) {
-                ks = 0;
-                k_phase ^= 1;
-              }
-            }
-#ifdef MMI_PROF
-            prof_nt += 2 * nh;
-#endif
-            if (live_cur & 1u) {
-              issue_pv(0, 2 * t);
-              issue_pv(0, 2 * t + 1);
-            }
-            if (ahead && (live_next & 1u)) issue_s128(0, knext);
-            if (b_deferred) {  // half B's first S, half a period behind half A
-              issue_s128(1, kcur);
-              b_deferred = false;
-              if (n == 1) umma_commit(q_empty);
-              umma_commit(k_empty + kcur);
-            }
-            if (nh > 1 && (live_cur & 2u)) {
-              issue_pv(1, 2 * t);
-              issue_pv(1, 2 * t + 1);
-            }
-            if (ahead) {
-              if (nh > 1 && (live_next & 2u)) issue_s128(1, knext);
-              if (t + 1 == n - 1) umma_commit(q_empty);  // last S of the item issued
-              umma_commit(k_empty + knext);
-            }
-            umma_commit(v_empty + vs);
-            if (++vs == VST) {
-              vs = 0;
-              v_phase ^= 1;
-            }
-            live_cur = live_next;
-          }
-#else
           t0 = PROF_T();
           mbar_wait(k_full + ks, k_phase);
           PROF_ADD(wk, t0);
@@ -743,63 +697,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             live_cur = live_next;
           }
-#endif
-#else
-          // prologue: both sub-tiles of key tile 0 for every live half
-          t0 = PROF_T();
-          mbar_wait(k_full + ks, k_phase);
-          PROF_ADD(wk, t0);
-          tc_fence_after();
-          uint32_t live_cur = (uint32_t)live_s[ks], live_next = 0;
-          for (int j = 0; j < 2; ++j)
-            for (int hf = 0; hf < nh; ++hf)
-              if ((live_cur >> hf) & 1u) issue_s(hf, j, ks);
-          if (nsub == 2) umma_commit(q_empty);  // last S of the item issued
-          umma_commit(k_empty + ks);
-          if (++ks == KST) {
-            ks = 0;
-            k_phase ^= 1;
-          }
-          for (int j = 0; j < nsub; ++j) {
-            const int u = j & 1;
-            const bool ahead = (j + 2 < nsub);  // S of sub-tile j + 2 (key tile t + 1, stage ks)
-            if (u == 0) {
-              t0 = PROF_T();
-              mbar_wait(v_full + vs, v_phase);
-              PROF_ADD(wv, t0);
-              if (ahead) {
-                t0 = PROF_T();
-                mbar_wait(k_full + ks, k_phase);
-                PROF_ADD(wk, t0);
-                tc_fence_after();
-                live_next = (uint32_t)live_s[ks];
-              }
-            }
-#ifdef MMI_PROF
-            prof_nt += nh;
-#endif
-            for (int hf = 0; hf < nh; ++hf) {
-              if ((live_cur >> hf) & 1u) issue_pv(hf, j);
-              if (ahead && ((live_next >> hf) & 1u)) issue_s(hf, j + 2, ks);
-            }
-            if (j + 2 == nsub - 1) umma_commit(q_empty);  // last S of the item issued
-            if (u == 1) {
-              umma_commit(v_empty + vs);
-              if (++vs == VST) {
-                vs = 0;
-                v_phase ^= 1;
-              }
-              if (ahead) {
-                umma_commit(k_empty + ks);
-                if (++ks == KST) {
-                  ks = 0;
-                  k_phase ^= 1;
-                }
-              }
-              live_cur = live_next;
-            }
-          }
-#endif
           // O_h complete for every half that issued a P V (a half with no live tile has no O)
           for (int hf = 0; hf < nh; ++hf)
             if ((started >> hf) & 1u) {
@@ -808,24 +705,37 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
         }
         PROF_ADD(tot, prof_start);
+#ifdef MMI_TRACE
+        if (blockIdx.x == 0) g_trace_n[0] = tr_n;
+#endif
         PROF_FLUSH(0, tot); PROF_FLUSH(1, wp); PROF_FLUSH(2, wk); PROF_FLUSH(3, wv); PROF_FLUSH(4, wq);
         PROF_FLUSH(5, wo); PROF_FLUSH(6, nt);
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SOFT_REGS));
-    // ======================= softmax / correction / epilogue (one warpgroup per half) =======================
-    const int hf = (warp - NWARP_CTRL) / 4;                 // half of the item this warpgroup owns
-    const int row = (threadIdx.x - 32 * NWARP_CTRL) % 128;  // TMEM lane == row of the half
+    if (SOFT_REGS > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SOFT_REGS > 0 ? SOFT_REGS : 256));
+    // ======================= softmax / correction / epilogue =======================
+    // HPW = 1: one warpgroup per half (8 warps); HPW = 2: one warpgroup does both halves, half A's
+    // sub-tiles then half B's (4 warps; the two halves never contend for MUFU on a sub-partition).
+    // Thread t owns TMEM lane t = row t of each of its halves.
+    const int h0 = (HPW == 1) ? (warp - NWARP_CTRL) / 4 : 0;  // first half this warpgroup owns
+    const int row = (threadIdx.x - 32 * NWARP_CTRL) % 128;     // TMEM lane == row of the half
     const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
-    const uint32_t tS = tmem + 128 * hf + lane_off;
-    const uint32_t tO = tmem + 256 + 128 * hf + lane_off;
     int kps = 0;  // key-coordinate ring
-    uint32_t kp_phase = 0, o_phase = 0;
-    uint32_t s_phase[2] = {0, 0};
+    uint32_t kp_phase = 0;
     int rs = 0;  // row-identity stage
     uint32_t rs_phase = 0;
-    uint32_t n_sub = 0;  // sub-tiles this half has processed (= P V commits on pv_done[hf])
+    // per-half pipeline phases (persist across items)
+    // pv_done[hf][u] completes once per P V of slot u.  After P(j) is handed over the softmax owes
+    // a wait on its phase (owe bit u); it pays it before its next rescale (which needs P(j) V to
+    // have landed), or at the S wait of sub-tile j + 2 (issued after P(j) V: returns at once), or
+    // at the O wait -- always before the slot's next commit, so no phase goes unobserved.
+    uint32_t s_phase[HPW], o_phase[HPW], pv_phase[HPW], owe[HPW];  // pv_phase / owe: bit u per slot
+#pragma unroll
+    for (int j = 0; j < HPW; ++j) {
+      s_phase[j] = 0;
+      o_phase[j] = pv_phase[j] = owe[j] = 0;
+    }
     const int G = P.H / P.Hkv;
     PROF_DECL(stot); PROF_DECL(sws); PROF_DECL(sld); PROF_DECL(smask); PROF_DECL(ssm); PROF_DECL(sresc);
     PROF_DECL(spst); PROF_DECL(sepi); PROF_DECL(snt); PROF_DECL(snr); PROF_DECL(sfetch); PROF_DECL(sitem); PROF_DECL(smword); PROF_DECL(sepw); PROF_DECL(sepl);
@@ -839,19 +749,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (idx < 0) break;
       const ItemView it = item_of(i, idx);
       if (it.n_tiles <= 0) continue;  // empty slot: nothing to compute or write
+      const int nh_mine = (HPW == 1) ? ((h0 == 0 || it.has_b) ? 1 : 0) : (it.has_b ? 2 : 1);
       // row identity (positions / ranks staged in shared memory by warp 0)
-      int xpos = it.q_row0 + hf * BLK + row - it.head * P.S, xrank = xpos;
+      int xpos[HPW], xrank[HPW];
+#pragma unroll
+      for (int j = 0; j < HPW; ++j) {
+        xpos[j] = it.q_row0 + (h0 + j) * BLK + row - it.head * P.S;
+        xrank[j] = xpos[j];
+      }
       if (!P.dense) {
         mbar_wait(ri_full + rs, rs_phase);
         const int32_t* rip = ri_s + rs * 4 * BLK;
-        const int li = hf * BLK + row;
-        if (it.q_gathered) {
-          xpos = rip[li];
-          xrank = rip[2 * BLK + li];
-        } else if (P.rank) {
-          const int x0 = it.q_row0 - it.head * P.S;
-          const int n4 = min((it.has_b ? 2 : 1) * BLK, P.S - x0) & ~3;
-          xrank = li < n4 ? rip[2 * BLK + li] : (xpos < P.S ? P.rank[xpos] : xpos);
+#pragma unroll
+        for (int j = 0; j < HPW; ++j) {
+          const int li = (h0 + j) * BLK + row;
+          if (it.q_gathered) {
+            xpos[j] = rip[li];
+            xrank[j] = rip[2 * BLK + li];
+          } else if (P.rank) {
+            const int x0 = it.q_row0 - it.head * P.S;
+            const int n4 = min((it.has_b ? 2 : 1) * BLK, P.S - x0) & ~3;
+            xrank[j] = li < n4 ? rip[2 * BLK + li] : (xpos[j] < P.S ? P.rank[xpos[j]] : xpos[j]);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(ri_empty + rs);
@@ -860,7 +779,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           rs_phase ^= 1;
         }
       }
-      if (hf == 1 && !it.has_b) {
+      if (nh_mine == 0) {
         // absent half: only release the key-coordinate stages
         SegIter si;
         si.init(P, it);
@@ -878,17 +797,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         continue;
       }
-      if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 3] = gtimer();
+      if (P.dbg && row == 0 && h0 == 0) P.dbg[idx * 8 + 3] = gtimer();
+      TR(9, 0);
       t0 = PROF_T();
-      bool valid = xpos >= 0 && xpos < P.S;
-      if (valid && it.row_mod >= 0) valid = (P.labels[xpos] == it.row_mod);
-      bool write = valid;
-      if (it.skip_s > 0 && valid) {
-        const int c = it.skip_rank ? xrank : xpos;
-        if (hline_row(c, it.skip_s, it.skip_p)) write = false;  // owned by the HROW pass
+      bool valid[HPW], write[HPW];
+      float m_used[HPW], l_sum[HPW];
+      long long fp_cnt[HPW], fp_s1[HPW], fp_s2[HPW];
+      int n_live[HPW];  // tiles of this item live for the half (= P V MMAs into O_h / 2)
+#pragma unroll
+      for (int j = 0; j < HPW; ++j) {
+        valid[j] = xpos[j] >= 0 && xpos[j] < P.S;
+        if (valid[j] && it.row_mod >= 0) valid[j] = (P.labels[xpos[j]] == it.row_mod);
+        write[j] = valid[j];
+        if (it.skip_s > 0 && valid[j]) {
+          const int c = it.skip_rank ? xrank[j] : xpos[j];
+          if (hline_row(c, it.skip_s, it.skip_p)) write[j] = false;  // owned by the HROW pass
+        }
+        m_used[j] = -INFINITY;
+        l_sum[j] = 0.f;
+        fp_cnt[j] = fp_s1[j] = fp_s2[j] = 0;
+        n_live[j] = 0;
       }
-      float m_used = -INFINITY, l_sum = 0.f;
-      long long fp_cnt = 0, fp_s1 = 0, fp_s2 = 0;
       const int kv = it.head / G;
       SegIter si;
       si.init(P, it);
@@ -896,359 +825,396 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t* c_sl = nullptr;
       const uint32_t* c_vm = nullptr;
       PROF_ADD(sitem, t0);
-      int n_live = 0;  // tiles of this item live for this half (= P V MMAs into O_h / 2)
-      auto release_kp = [&]() {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(kp_empty + kps);  // key coordinates of this stage consumed
-        if (++kps == NKP) {
-          kps = 0;
-          kp_phase ^= 1;
-        }
-      };
       for (int t = 0; t < it.n_tiles; ++t) {
         const TileInfo e = si.next(P, it);
-        const uint32_t my_st = e.st(hf);
         // the K loader staged this tile's key coordinates for whichever half masks it
         const bool kp_stage = e.space && (e.pred_any() || P.fingerprint);
-        if (my_st == TS_DEAD) {  // no admitted element for these rows: no S, no P V for this half
-          if (kp_stage) {
-            mbar_wait(kp_full + kps, kp_phase);
-            release_kp();
-          }
-          continue;
-        }
-        ++n_live;
-        const uint32_t space = e.space, pred = (my_st == TS_PRED) ? 1u : 0u, role = e.role, rmode = e.rmode,
-                       inst = e.inst;
-        const bool masked = pred || P.fingerprint;
-        uint32_t mw[4] = {0u, 0u, 0u, 0u};  // admitted-key mask of the tile (bit c <-> key c)
+        const uint32_t space = e.space, role = e.role, rmode = e.rmode, inst = e.inst;
+        uint32_t mw[HPW][4];  // admitted-key mask of the tile per half (bit c <-> key c)
         t0 = PROF_T();
-        if (!masked && kp_stage) {  // staged for the other half only
-          mbar_wait(kp_full + kps, kp_phase);
-          release_kp();
-        }
-        if (masked) {
-          const bool need_kp = kp_stage;
-          if (need_kp) mbar_wait(kp_full + kps, kp_phase);
-          const int* kp = kpos_s + kps * BLK;
-          if (valid) {
-            const int kbase = e.krow - kv * P.S;
-            if (!pred) {
-              range_mask(mw, 0, BLK - 1);
-            } else if (role == R_NAT) {
-              natten_mask(P, xpos, e.krow, mw);
-            } else {
-              if (!P.dense && role != R_TRUE && (int)inst != c_inst) {
-                // pattern parameters of the tile's instance: reloaded only when the instance changes
-                const InstParam ip = P.insts[it.inst_base + inst];
-                c_inst = (int)inst;
-                c_sink = ip.sink;
-                c_local = ip.local;
-                c_sl = ip.slash_word >= 0 ? P.bits + ip.slash_word : nullptr;
-                c_vm = ip.vmask_word >= 0 ? P.bits + ip.vmask_word : nullptr;
-              }
-              const int sink = c_sink, local = c_local;
-              const uint32_t* sl_bits = c_sl;
-              const uint32_t* vm_bits = c_vm;
-              const int x = rmode ? xrank : xpos;
-              // Keys of every view are ascending inside a tile, so each role is at most two
-              // index ranges: [0, n_causal) intersected with the pattern's coordinate ranges.
-              int n_causal, n_sink, n_lt_local, ybase;
-              const int thr = a_thr(x, local);  // keys y <= thr are outside the local part
-              if (!space) {
-                n_causal = min(max(xpos - kbase + 1, 0), BLK);
-                n_sink = min(max(sink - kbase, 0), BLK);
-                n_lt_local = min(max(thr - kbase + 1, 0), BLK);
-                ybase = kbase;
-              } else {
-                const int* yc = rmode ? (krank_s + kps * BLK) : kp;
-                if (role == R_A || role == R_NOTA) {
-                  count_le3(kp, xpos, yc, sink - 1, thr, n_causal, n_sink, n_lt_local);
-                } else {
-                  n_causal = count_le(kp, xpos);
-                  n_sink = n_lt_local = 0;
-                }
-                ybase = yc[0];
-              }
-              if (role == R_TRUE) {
-                range_mask(mw, 0, n_causal - 1);
-              } else if (role == R_A) {
-                range_mask(mw, 0, min(n_sink, n_causal) - 1);
-                range_mask(mw, n_lt_local, n_causal - 1);
-              } else if (role == R_NOTA) {
-                range_mask(mw, n_sink, min(n_lt_local, n_causal) - 1);
-              } else {
-                // vertical-slash: coordinates contiguous in the tile (original K, or a modality's
-                // rank-ordered keys); slash bits of offsets x - ybase - c, bit-reversed window
-                range_mask(mw, 0, n_causal - 1);
-                uint32_t ws[4], wv[4];
-                bit_window(sl_bits, x - ybase - (BLK - 1), ws);
-                bit_window(vm_bits, ybase, wv);
+        if (kp_stage) mbar_wait(kp_full + kps, kp_phase);
+        const int* kp = kpos_s + kps * BLK;
 #pragma unroll
-                for (int w = 0; w < 4; ++w) mw[w] &= __brev(ws[3 - w]) & ~wv[w];
-              }
+        for (int j = 0; j < HPW; ++j) {
+          mw[j][0] = mw[j][1] = mw[j][2] = mw[j][3] = 0u;
+          const int hf = h0 + j;
+          if (j >= nh_mine) continue;
+          const uint32_t my_st = e.st(hf);
+          if (my_st == TS_DEAD) continue;
+          const uint32_t pred = (my_st == TS_PRED) ? 1u : 0u;
+          if (!(pred || P.fingerprint) || !valid[j]) continue;
+          const int kbase = e.krow - kv * P.S;
+          if (!pred) {
+            range_mask(mw[j], 0, BLK - 1);
+          } else if (role == R_NAT) {
+            natten_mask(P, xpos[j], e.krow, mw[j]);
+          } else {
+            if (!P.dense && role != R_TRUE && (int)inst != c_inst) {
+              // pattern parameters of the tile's instance: reloaded only when the instance changes
+              const InstParam ip = P.insts[it.inst_base + inst];
+              c_inst = (int)inst;
+              c_sink = ip.sink;
+              c_local = ip.local;
+              c_sl = ip.slash_word >= 0 ? P.bits + ip.slash_word : nullptr;
+              c_vm = ip.vmask_word >= 0 ? P.bits + ip.vmask_word : nullptr;
             }
-            if (P.fingerprint) {
+            const int sink = c_sink, local = c_local;
+            const int x = rmode ? xrank[j] : xpos[j];
+            // Keys of every view are ascending inside a tile, so each role is at most two
+            // index ranges: [0, n_causal) intersected with the pattern's coordinate ranges.
+            int n_causal, n_sink, n_lt_local, ybase;
+            const int thr = a_thr(x, local);  // keys y <= thr are outside the local part
+            if (!space) {
+              n_causal = min(max(xpos[j] - kbase + 1, 0), BLK);
+              n_sink = min(max(sink - kbase, 0), BLK);
+              n_lt_local = min(max(thr - kbase + 1, 0), BLK);
+              ybase = kbase;
+            } else {
+              const int* yc = rmode ? (krank_s + kps * BLK) : kp;
+              if (role == R_A || role == R_NOTA) {
+                count_le3(kp, xpos[j], yc, sink - 1, thr, n_causal, n_sink, n_lt_local);
+              } else {
+                n_causal = count_le(kp, xpos[j]);
+                n_sink = n_lt_local = 0;
+              }
+              ybase = yc[0];
+            }
+            if (role == R_TRUE) {
+              range_mask(mw[j], 0, n_causal - 1);
+            } else if (role == R_A) {
+              range_mask(mw[j], 0, min(n_sink, n_causal) - 1);
+              range_mask(mw[j], n_lt_local, n_causal - 1);
+            } else if (role == R_NOTA) {
+              range_mask(mw[j], n_sink, min(n_lt_local, n_causal) - 1);
+            } else {
+              // vertical-slash: coordinates contiguous in the tile (original K, or a modality's
+              // rank-ordered keys); slash bits of offsets x - ybase - c, bit-reversed window
+              range_mask(mw[j], 0, n_causal - 1);
+              uint32_t ws[4], wv[4];
+              bit_window(c_sl, x - ybase - (BLK - 1), ws);
+              bit_window(c_vm, ybase, wv);
 #pragma unroll
-              for (int w = 0; w < 4; ++w) {
-                uint32_t bitsw = mw[w];
-                while (bitsw) {
-                  const int c = w * 32 + __ffs(bitsw) - 1;
-                  bitsw &= bitsw - 1;
-                  const long long ypos = space ? kp[c] : kbase + c;
-                  fp_cnt += 1;
-                  fp_s1 += ypos;
-                  fp_s2 += ypos * ypos;
-                }
+              for (int w = 0; w < 4; ++w) mw[j][w] &= __brev(ws[3 - w]) & ~wv[w];
+            }
+          }
+          if (P.fingerprint) {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              uint32_t bitsw = mw[j][w];
+              while (bitsw) {
+                const int c = w * 32 + __ffs(bitsw) - 1;
+                bitsw &= bitsw - 1;
+                const long long ypos = space ? kp[c] : kbase + c;
+                fp_cnt[j] += 1;
+                fp_s1[j] += ypos;
+                fp_s2[j] += ypos * ypos;
               }
             }
           }
-          if (need_kp) release_kp();
+        }
+        if (kp_stage) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(kp_empty + kps);  // key coordinates of this stage consumed
+          if (++kps == NKP) {
+            kps = 0;
+            kp_phase ^= 1;
+          }
         }
         PROF_ADD(smword, t0);
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          t0 = PROF_T();
-          mbar_wait(s_full + 2 * hf + u, s_phase[u]);
-          PROF_ADD(sws, t0);
-          t0 = PROF_T();
-          s_phase[u] ^= 1;
-          tc_fence_after();
-#ifdef MMI_NOSOFT
-          // pipeline ceiling experiment (scratch builds only): no softmax work at all
-          tc_fence_before();
-          mbar_arrive(p_full + 2 * hf + u);
-          ++n_sub;
-          continue;
-#endif
-          float s[64];
+        for (int j = 0; j < HPW; ++j) {
+          const int hf = h0 + j;
+          if (j >= nh_mine) continue;
+          const uint32_t my_st = e.st(hf);
+          if (my_st == TS_DEAD) continue;  // no admitted element for these rows: no S, no P V for this half
+          ++n_live[j];
+          const bool masked = (my_st == TS_PRED) || P.fingerprint;
+          const uint32_t tS = tmem + 128 * hf + lane_off;
+          const uint32_t tO = tmem + 256 + 128 * hf + lane_off;
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tS + 64 * u + c * 32, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(r[j]);  // raw scores
-          }
-          PROF_ADD(sld, t0);
-          t0 = PROF_T();
-          // (sub-tiles every row of the warp fully admits skip the select: diagonal / sink / local
-          // tiles are mostly all-or-nothing per 64 keys)
-#ifdef MMI_NO_MASKSKIP
-          if (masked) {
-#else
-          if (masked && !__all_sync(0xffffffffu, (mw[2 * u] & mw[2 * u + 1]) == 0xffffffffu)) {
-#endif
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (!((mw[2 * u + (c >> 5)] >> (c & 31)) & 1u)) s[c] = -INFINITY;
-          }
-          PROF_ADD(smask, t0);
-          t0 = PROF_T();
-          // ---- online softmax (log2 domain), lazy rescale ----
-          float mx[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) mx[j] = fmaxf(s[j], s[j + 8]);
-#pragma unroll
-          for (int c = 16; c < 64; c += 16)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) mx[j] = fmaxf(mx[j], fmaxf(s[c + j], s[c + 8 + j]));
-          float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-          if (mt > -INFINITY) mt *= P.scale_log2;  // tau * log2(e) > 0 commutes with max
-          float alpha = 1.f;
-          bool rescale = false;
-          if (mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt > -INFINITY)) {
-            alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mt);
-            rescale = (m_used != -INFINITY);
-            m_used = mt;
-          }
-          const float mu = (m_used == -INFINITY) ? 0.f : m_used;
-          const float2 sc2 = make_float2(P.scale_log2, P.scale_log2), nmu2 = make_float2(-mu, -mu);
-          float2 ls2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                           make_float2(0.f, 0.f)};
-          uint32_t pk[32];
-#pragma unroll
-          for (int c = 0; c < 64; c += 2) {
-            const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nmu2);
-            float2 pr;
-            if ((EMU_MASK >> ((c / 2) % 8)) & 1u) {
-              pr = exp2_poly2(x);
-            } else {
-              pr.x = ex2(x.x);
-              pr.y = ex2(x.y);
+          for (int u = 0; u < 2; ++u) {
+            t0 = PROF_T();
+            if (u == 0) {  // S of both 64-key slots landed together (one M128 N128 group)
+              mbar_wait(s_full + 2 * hf, s_phase[j]);
+              s_phase[j] ^= 1;
             }
-            ls2[(c / 2) % 4] = fadd2(ls2[(c / 2) % 4], pr);
-            pk[c / 2] = pack_bf16(pr.x, pr.y);
-          }
-          const float2 lsa = fadd2(fadd2(ls2[0], ls2[1]), fadd2(ls2[2], ls2[3]));
-          l_sum = l_sum * alpha + (lsa.x + lsa.y);
-          PROF_ADD(ssm, t0);
-          t0 = PROF_T();
-          // O correction only when the running max moved (rare).  P V of the previous sub-tile
-          // may still be in flight (S of this sub-tile was issued before it): wait for it.
-          if (__any_sync(0xffffffffu, rescale)) {
-            mbar_wait(pv_done + hf, (n_sub - 1) & 1);
+            PROF_ADD(sws, t0);
+            TR(4, u);
+            t0 = PROF_T();
+            if ((owe[j] >> u) & 1u) {  // S(j) was issued after P(j - 2) V: returns at once
+              mbar_wait(pv_done + 2 * hf + u, (pv_phase[j] >> u) & 1u);
+              pv_phase[j] ^= 1u << u;
+              owe[j] &= ~(1u << u);
+            }
             tc_fence_after();
+#ifdef MMI_NOSOFT
+            // pipeline ceiling experiment (scratch builds only): no softmax work at all
+            tc_fence_before();
+            mbar_arrive(p_full + 2 * hf + u);
+            owe[j] |= 1u << u;
+            continue;
+#endif
+            float s[64];
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
+            for (int c = 0; c < 2; ++c) {
               uint32_t r[32];
-              tmem_ld32(tO + c * 32, r);
+              tmem_ld32(tS + 64 * u + c * 32, r);
               tmem_wait_ld();
 #pragma unroll
-              for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
-              tmem_st32(tO + c * 32, r);
+              for (int q = 0; q < 32; ++q) s[c * 32 + q] = __uint_as_float(r[q]);  // raw scores
             }
+            PROF_ADD(sld, t0);
+            t0 = PROF_T();
+            // (sub-tiles every row of the warp fully admits skip the select: diagonal / sink / local
+            // tiles are mostly all-or-nothing per 64 keys)
+            if (masked && !__all_sync(0xffffffffu, (mw[j][2 * u] & mw[j][2 * u + 1]) == 0xffffffffu)) {
+#pragma unroll
+              for (int c = 0; c < 64; ++c)
+                if (!((mw[j][2 * u + (c >> 5)] >> (c & 31)) & 1u)) s[c] = -INFINITY;
+            }
+            PROF_ADD(smask, t0);
+            t0 = PROF_T();
+            // ---- online softmax (log2 domain), lazy rescale ----
+            float mx[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) mx[q] = fmaxf(s[q], s[q + 8]);
+#pragma unroll
+            for (int c = 16; c < 64; c += 16)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) mx[q] = fmaxf(mx[q], fmaxf(s[c + q], s[c + 8 + q]));
+            float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                             fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+            if (mt > -INFINITY) mt *= P.scale_log2;  // tau * log2(e) > 0 commutes with max
+            float alpha = 1.f;
+            bool rescale = false;
+            if (mt > m_used[j] + RESCALE_THRESH || (m_used[j] == -INFINITY && mt > -INFINITY)) {
+              alpha = (m_used[j] == -INFINITY) ? 0.f : ex2(m_used[j] - mt);
+              rescale = (m_used[j] != -INFINITY);
+              m_used[j] = mt;
+            }
+            const float mu = (m_used[j] == -INFINITY) ? 0.f : m_used[j];
+            const float2 sc2 = make_float2(P.scale_log2, P.scale_log2), nmu2 = make_float2(-mu, -mu);
+            float2 ls2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                             make_float2(0.f, 0.f)};
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < 64; c += 2) {
+              const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nmu2);
+              float2 pr;
+              if ((EMU_MASK >> ((c / 2) % 8)) & 1u) {
+                pr = exp2_poly2(x);
+              } else {
+                pr.x = ex2(x.x);
+                pr.y = ex2(x.y);
+              }
+              ls2[(c / 2) % 4] = fadd2(ls2[(c / 2) % 4], pr);
+              pk[c / 2] = pack_bf16(pr.x, pr.y);
+              // first 32 keys of P on their way to TMEM while the rest is exponentiated
+              if (c == 30) tmem_st16(tS + 64 * u, pk);
+            }
+            const float2 lsa = fadd2(fadd2(ls2[0], ls2[1]), fadd2(ls2[2], ls2[3]));
+            l_sum[j] = l_sum[j] * alpha + (lsa.x + lsa.y);
+            PROF_ADD(ssm, t0);
+            TR(5, u);
+            t0 = PROF_T();
+            // O correction only when the running max moved (rare): P(j - 1) V may still be in flight
+            const bool any_rescale = __any_sync(0xffffffffu, rescale);
+            if (any_rescale && ((owe[j] >> (u ^ 1)) & 1u)) {
+              mbar_wait(pv_done + 2 * hf + (u ^ 1), (pv_phase[j] >> (u ^ 1)) & 1u);
+              pv_phase[j] ^= 1u << (u ^ 1);
+              owe[j] &= ~(1u << (u ^ 1));
+            }
+            if (any_rescale) {
+              tc_fence_after();
+#pragma unroll
+              for (int c = 0; c < D / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tO + c * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int q = 0; q < 32; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * alpha);
+                tmem_st32(tO + c * 32, r);
+              }
 #ifdef MMI_PROF
-            prof_snr += 1;
+              prof_snr += 1;
+#endif
+            }
+            PROF_ADD(sresc, t0);
+            t0 = PROF_T();
+            // P (bf16 pairs) -> TMEM columns [64u, 64u + 32) of this half's S buffer
+            tmem_st16(tS + 64 * u + 16, pk + 16);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(p_full + 2 * hf + u);
+            owe[j] |= 1u << u;  // P(j) V will complete a phase of pv_done[hf][u]
+            PROF_ADD(spst, t0);
+            TR(6, u);
+#ifdef MMI_PROF
+            prof_snt += 1;
 #endif
           }
-          PROF_ADD(sresc, t0);
-          t0 = PROF_T();
-          // P (bf16 pairs) -> TMEM columns [64u, 64u + 32) of this half's S buffer
-          tmem_st32(tS + 64 * u, pk);
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(p_full + 2 * hf + u);
-          ++n_sub;
-          PROF_ADD(spst, t0);
-#ifdef MMI_PROF
-          prof_snt += 1;
-#endif
         }
       }
-      t0 = PROF_T();
       // ---- epilogue ----  (a half with no live tile in this item has no O: it writes zeros / -inf)
-      const bool has_o = n_live > 0;
-      if (has_o) {
-        mbar_wait(o_full + hf, o_phase);
-        o_phase ^= 1;
-        tc_fence_after();
-      }
-      PROF_ADD(sepw, t0);
-      // no admitted key in this item <=> the running max never left -inf (the polynomial exp2
-      // maps masked scores to 2^-125, so l_sum alone does not tell)
-      if (m_used == -INFINITY) l_sum = 0.f;
-      const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
-      const float lse_v = l_sum > 0.f ? (m_used + __log2f(l_sum)) * 0.6931471805599453f : -INFINITY;
-      if (P.fingerprint) {
+#pragma unroll
+      for (int j = 0; j < HPW; ++j) {
+        const int hf = h0 + j;
+        if (j >= nh_mine) continue;
+        const uint32_t tO = tmem + 256 + 128 * hf + lane_off;
+        t0 = PROF_T();
+        const bool has_o = n_live[j] > 0;
+        TR(7, 0);
         if (has_o) {
-          tc_fence_before();
-          mbar_arrive(o_empty + hf);
+          mbar_wait(o_full + hf, o_phase[j]);
+          o_phase[j] ^= 1;
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if ((owe[j] >> u) & 1u) {  // O_h complete: every P V of the item has landed
+              mbar_wait(pv_done + 2 * hf + u, (pv_phase[j] >> u) & 1u);
+              pv_phase[j] ^= 1u << u;
+            }
+          owe[j] = 0;
+          tc_fence_after();
         }
-        if (write) {
-          long long* f = reinterpret_cast<long long*>(P.fp_out) + 3ll * ((long long)it.head * P.S + xpos);
-          atomicAdd(reinterpret_cast<unsigned long long*>(f + 0), (unsigned long long)fp_cnt);
-          atomicAdd(reinterpret_cast<unsigned long long*>(f + 1), (unsigned long long)fp_s1);
-          atomicAdd(reinterpret_cast<unsigned long long*>(f + 2), (unsigned long long)fp_s2);
+        PROF_ADD(sepw, t0);
+        TR(10, 0);
+        // no admitted key in this item <=> the running max never left -inf (the polynomial exp2
+        // maps masked scores to 2^-125, so l_sum alone does not tell)
+        const float lsum = (m_used[j] == -INFINITY) ? 0.f : l_sum[j];
+        const float inv_l = lsum > 0.f ? 1.f / lsum : 0.f;
+        const float lse_v = lsum > 0.f ? (m_used[j] + __log2f(lsum)) * 0.6931471805599453f : -INFINITY;
+        if (P.fingerprint) {
+          if (has_o) {
+            tc_fence_before();
+            mbar_arrive(o_empty + hf);
+          }
+          if (write[j]) {
+            long long* f = reinterpret_cast<long long*>(P.fp_out) + 3ll * ((long long)it.head * P.S + xpos[j]);
+            atomicAdd(reinterpret_cast<unsigned long long*>(f + 0), (unsigned long long)fp_cnt[j]);
+            atomicAdd(reinterpret_cast<unsigned long long*>(f + 1), (unsigned long long)fp_s1[j]);
+            atomicAdd(reinterpret_cast<unsigned long long*>(f + 2), (unsigned long long)fp_s2[j]);
+          }
+          continue;
         }
-        continue;
-      }
-      // O (fp32, TMEM) -> 16-bit registers: bf16 for final rows, fp16 for partial rows (merged in fp32
-      // by merge_kernel).  O is released as soon as it is in registers.
-      const bool fin = (it.out_mode == OUT_FINAL);
-      uint32_t ov[D / 2];
+        // O (fp32, TMEM) -> 16-bit registers: bf16 for final rows, fp16 for partial rows (merged in
+        // fp32 by merge_kernel).  O is released as soon as it is in registers.
+        const bool fin = (it.out_mode == OUT_FINAL);
+        uint32_t ov[D / 2];
 #pragma unroll
-      for (int c = 0; c < D / 32; c += 2) {  // two 32-column loads in flight per wait
-        uint32_t r[2][32];
-        if (has_o) {
-          tmem_ld32(tO + c * 32, r[0]);
-          tmem_ld32(tO + c * 32 + 32, r[1]);
-          tmem_wait_ld();
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) r[0][j] = r[1][j] = 0u;
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (fin) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              ov[(c + h) * 16 + j] =
-                  pack_bf16(__uint_as_float(r[h][2 * j]) * inv_l, __uint_as_float(r[h][2 * j + 1]) * inv_l);
+        for (int c = 0; c < D / 32; c += 2) {  // two 32-column loads in flight per wait
+          uint32_t r[2][32];
+          if (has_o) {
+            tmem_ld32(tO + c * 32, r[0]);
+            tmem_ld32(tO + c * 32 + 32, r[1]);
+            tmem_wait_ld();
           } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              ov[(c + h) * 16 + j] =
-                  pack_f16(__uint_as_float(r[h][2 * j]) * inv_l, __uint_as_float(r[h][2 * j + 1]) * inv_l);
+            for (int q = 0; q < 32; ++q) r[0][q] = r[1][q] = 0u;
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (fin) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                ov[(c + h) * 16 + q] =
+                    pack_bf16(__uint_as_float(r[h][2 * q]) * inv_l, __uint_as_float(r[h][2 * q + 1]) * inv_l);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                ov[(c + h) * 16 + q] =
+                    pack_f16(__uint_as_float(r[h][2 * q]) * inv_l, __uint_as_float(r[h][2 * q + 1]) * inv_l);
+            }
           }
         }
-      }
-      if (has_o) {
-        tc_fence_before();
-        mbar_arrive(o_empty + hf);  // the next item's first P V of this half may start
-      }
-      PROF_ADD(sepl, t0);
-      // destination row (0: not written).  Partial rows are always written (zeros for invalid rows:
-      // the merge weights them by exp(-inf) = 0, which must not meet a NaN).
-      unsigned long long dst = 0;
-      if (fin) {
-        if (write) dst = reinterpret_cast<unsigned long long>(reinterpret_cast<__nv_bfloat16*>(P.o) +
-                                                              ((size_t)it.head * P.S + xpos) * D);
-      } else {
-        dst = reinterpret_cast<unsigned long long>(P.part_o + (size_t)(it.out_row0 + hf * BLK + row) * D);
-      }
-      const uint32_t ebuf = smem_u32(smem + L::OFF_EPI + (warp - NWARP_CTRL) * 32 * EPI_STRIDE);
-      const int wrow0 = (warp % 4) * 32;  // first row of this warp in the half (its TMEM lane base)
-      if (!fin || (!it.q_gathered && __all_sync(0xffffffffu, write))) {
-        // The warp's 32 rows are contiguous in the destination (partial rows, or final rows of an
-        // original-order block that are all written): each 16-column chunk (32 rows x 32 B) is
-        // staged in the TMA 32B-swizzle layout (16 B half q of row r at q ^ ((r >> 2) & 1):
-        // conflict-free) in one of two 1 KB buffers and written by one asynchronous TMA tensor
-        // store; a buffer is refilled once the store two chunks back has read it.
-        const CUtensorMap* tm = fin ? &tmO : &tmPart;
-        const int grow = (fin ? it.q_row0 : it.out_row0) + hf * BLK + wrow0;
+        if (has_o) {
+          tc_fence_before();
+          mbar_arrive(o_empty + hf);  // the next item's first P V of this half may start
+        }
+        PROF_ADD(sepl, t0);
+        TR(11, fin ? (it.q_gathered ? 1 : 0) : 2);
+        t0 = PROF_T();
+#ifdef MMI_NOEPI
+        continue;  // pipeline ceiling experiment (scratch builds only): no output stores
+#endif
+        // destination row (0: not written).  Partial rows are always written (zeros for invalid
+        // rows: the merge weights them by exp(-inf) = 0, which must not meet a NaN).
+        unsigned long long dst = 0;
+        if (fin) {
+          if (write[j]) dst = reinterpret_cast<unsigned long long>(reinterpret_cast<__nv_bfloat16*>(P.o) +
+                                                                   ((size_t)it.head * P.S + xpos[j]) * D);
+        } else {
+          dst = reinterpret_cast<unsigned long long>(P.part_o + (size_t)(it.out_row0 + hf * BLK + row) * D);
+        }
+        const uint32_t ebuf = smem_u32(smem + L::OFF_EPI + (warp - NWARP_CTRL) * 32 * EPI_STRIDE);
+        const int wrow0 = (warp % 4) * 32;  // first row of this warp in the half (its TMEM lane base)
+#ifdef MMI_EPI_NOTMA
+        if (false) {
+#else
+        if (!fin || (!it.q_gathered && __all_sync(0xffffffffu, write[j]))) {
+#endif
+          // The warp's 32 rows are contiguous in the destination (partial rows, or final rows of an
+          // original-order block that are all written): each 16-column chunk (32 rows x 32 B) is
+          // staged in the TMA 32B-swizzle layout (16 B half q of row r at q ^ ((r >> 2) & 1):
+          // conflict-free) in one of two 1 KB buffers and written by one asynchronous TMA tensor
+          // store; a buffer is refilled once the store two chunks back has read it.
+          const CUtensorMap* tm = fin ? &tmO : &tmPart;
+          const int grow = (fin ? it.q_row0 : it.out_row0) + hf * BLK + wrow0;
 #pragma unroll
-        for (int c = 0; c < D / 16; ++c) {
-          const uint32_t buf = ebuf + (c & 1) * 1024;
-          if (c >= 2) {
-            if (lane == 0) bulk_wait_read1();
+          for (int c = 0; c < D / 16; ++c) {
+            const uint32_t buf = ebuf + (c & 1) * 1024;
+            if (c >= 2) {
+              if (lane == 0) bulk_wait_read1();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              st_shared_v4(buf + lane * 32 + ((q ^ ((lane >> 2) & 1)) * 16), ov[c * 8 + 4 * q],
+                           ov[c * 8 + 4 * q + 1], ov[c * 8 + 4 * q + 2], ov[c * 8 + 4 * q + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(tm, buf, c * 16, grow);
+              bulk_commit();
+            }
+          }
+          if (lane == 0) bulk_wait_read0();  // staging buffers free for the next item / half
+          __syncwarp();
+        } else {
+          // scattered rows: thread-per-row stores would touch 32 rows (32 L1 wavefronts) per
+          // instruction; instead each 64-byte column chunk of the warp's 32 rows is transposed
+          // through shared memory so that one 16-byte store instruction writes 8 rows x 64 B.
+          unsigned long long dsts[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) dsts[k] = __shfl_sync(0xffffffffu, dst, k * 8 + (lane >> 2));
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_shared_v4(ebuf + lane * EPI_STRIDE + q * 16, ov[c * 16 + 4 * q], ov[c * 16 + 4 * q + 1],
+                           ov[c * 16 + 4 * q + 2], ov[c * 16 + 4 * q + 3]);
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint4 w = ld_shared_v4(ebuf + (k * 8 + (lane >> 2)) * EPI_STRIDE + (lane & 3) * 16);
+              if (dsts[k]) *reinterpret_cast<uint4*>(dsts[k] + c * 64 + (lane & 3) * 16) = w;
+            }
             __syncwarp();
           }
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            st_shared_v4(buf + lane * 32 + ((q ^ ((lane >> 2) & 1)) * 16), ov[c * 8 + 4 * q], ov[c * 8 + 4 * q + 1],
-                         ov[c * 8 + 4 * q + 2], ov[c * 8 + 4 * q + 3]);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(tm, buf, c * 16, grow);
-            bulk_commit();
-          }
         }
-        if (lane == 0) bulk_wait_read0();  // staging buffers free for the next item
-        __syncwarp();
-      } else {
-        // scattered rows: thread-per-row stores would touch 32 rows (32 L1 wavefronts) per
-        // instruction; instead each 64-byte column chunk of the warp's 32 rows is transposed through
-        // shared memory so that one 16-byte store instruction writes 8 rows x 64 contiguous bytes.
-        unsigned long long dsts[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) dsts[k] = __shfl_sync(0xffffffffu, dst, k * 8 + (lane >> 2));
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            st_shared_v4(ebuf + lane * EPI_STRIDE + q * 16, ov[c * 16 + 4 * q], ov[c * 16 + 4 * q + 1],
-                         ov[c * 16 + 4 * q + 2], ov[c * 16 + 4 * q + 3]);
-          __syncwarp();
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint4 w = ld_shared_v4(ebuf + (k * 8 + (lane >> 2)) * EPI_STRIDE + (lane & 3) * 16);
-            if (dsts[k]) *reinterpret_cast<uint4*>(dsts[k] + c * 64 + (lane & 3) * 16) = w;
-          }
-          __syncwarp();
+        if (fin) {
+          if (write[j] && P.lse) P.lse[(size_t)it.head * P.S + xpos[j]] = lse_v;
+        } else {
+          P.part_lse[it.out_row0 + hf * BLK + row] = valid[j] ? lse_v : -INFINITY;
         }
+        if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 6] = gtimer();
+        PROF_ADD(sepi, t0);
+        TR(8, 0);
       }
-      if (fin) {
-        if (write && P.lse) P.lse[(size_t)it.head * P.S + xpos] = lse_v;
-      } else {
-        P.part_lse[it.out_row0 + hf * BLK + row] = valid ? lse_v : -INFINITY;
-      }
-      if (P.dbg && row == 0 && hf == 0) P.dbg[idx * 8 + 6] = gtimer();
-      PROF_ADD(sepi, t0);
     }
     if (lane == 0) bulk_wait0();  // this warp's TMA output stores are complete
+#ifdef MMI_TRACE
+    if (blockIdx.x == 0 && tr_reg > 0) g_trace_n[tr_reg] = tr_n;
+#endif
     PROF_ADD(stot, sprof_start);
     if (lane == 0) {
       PROF_FLUSH(8, stot); PROF_FLUSH(9, sws); PROF_FLUSH(10, sld); PROF_FLUSH(11, smask); PROF_FLUSH(12, ssm);
@@ -1265,6 +1231,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // ------------------------------------------------------------------ host side
+#ifdef MMI_TRACE
+extern "C" __attribute__((visibility("default"))) int mmi_debug_trace(unsigned long long* out, int* n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
+  cudaMemcpyFromSymbol(n, g_trace_n, sizeof(g_trace_n));
+  return 0;
+}
+#endif
 #ifdef MMI_PROF
 extern "C" __attribute__((visibility("default"))) int mmi_debug_prof(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
