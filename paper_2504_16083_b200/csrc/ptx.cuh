@@ -50,8 +50,13 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef MMI_SPIN
+  while (!mbar_test_wait(bar, parity)) {  // experiment: non-suspending poll
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // shared-window (u32) address forms, for loops that keep barrier addresses in registers

@@ -168,8 +168,12 @@ __global__ void __launch_bounds__(STC_THREADS, 2)
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     if (mode == 0) {
       // ---- pass 1: TMEM lane = slab row r; running max / normaliser over this chunk's keys ----
+      // 64 columns per step (two 32-column loads in flight per wait), one max and one rescale per
+      // step, packed FFMA2 for the scaled scores; the causal select only where a row's admitted
+      // keys end inside the step
       const bool valid = my_pos >= 0;
       float m = -INFINITY, l = 0.f;
+      const float2 sc2 = make_float2(scale_log2, scale_log2);
       for (int i = 0; i < nt; ++i) {
         const int b = i & 1;
         const int j0 = (t_begin + i) * BLK;
@@ -178,25 +182,40 @@ __global__ void __launch_bounds__(STC_THREADS, 2)
         // keys j0 + c admitted for this row iff j0 + c <= pos (causal; pos < S)
         const int n_ok = valid ? min(max(my_pos - j0 + 1, 0), BLK) : 0;
 #pragma unroll
-        for (int c = 0; c < BLK / 32; ++c) {
-          uint32_t raw[32];
-          tmem_ld32(tmem + b * 128 + c * 32 + lane_off, raw);
+        for (int h = 0; h < 2; ++h) {
+          uint32_t raw[2][32];
+          tmem_ld32(tmem + b * 128 + h * 64 + lane_off, raw[0]);
+          tmem_ld32(tmem + b * 128 + h * 64 + 32 + lane_off, raw[1]);
           tmem_wait_ld();
-          float v[32];
-          float mx = -INFINITY;
+          const int lim = n_ok - h * 64;  // admitted columns of this step: [0, lim) (none if <= 0)
+          float v[64];
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            v[k] = (c * 32 + k < n_ok) ? __uint_as_float(raw[k]) * scale_log2 : -INFINITY;
-            mx = fmaxf(mx, v[k]);
-          }
-          const float mn = fmaxf(m, mx);
-          if (mn > -INFINITY) {
-            float sum = 0.f;
+          for (int k = 0; k < 64; ++k) v[k] = __uint_as_float(raw[k / 32][k % 32]);
+          if (__any_sync(0xffffffffu, lim < 64)) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) sum += ex2(v[k] - mn);
-            l = (m > -INFINITY ? l * ex2(m - mn) : 0.f) + sum;
-            m = mn;
+            for (int k = 0; k < 64; ++k) v[k] = (k < lim) ? v[k] : -INFINITY;
           }
+          float mx[4] = {v[0], v[1], v[2], v[3]};
+#pragma unroll
+          for (int k = 4; k < 64; k += 4) {
+            mx[0] = fmaxf(mx[0], v[k]);
+            mx[1] = fmaxf(mx[1], v[k + 1]);
+            mx[2] = fmaxf(mx[2], v[k + 2]);
+            mx[3] = fmaxf(mx[3], v[k + 3]);
+          }
+          const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;  // scale > 0
+          const float mn = fmaxf(m, mt);
+          const float mu = (mn == -INFINITY) ? 0.f : mn;  // no admitted key yet: every term is 0
+          const float2 nm2 = make_float2(-mu, -mu);
+          float2 s2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int k = 0; k < 64; k += 2) {
+            const float2 x = ffma2(make_float2(v[k], v[k + 1]), sc2, nm2);
+            s2[(k / 2) % 4] = fadd2(s2[(k / 2) % 4], make_float2(ex2(x.x), ex2(x.y)));
+          }
+          const float2 st = fadd2(fadd2(s2[0], s2[1]), fadd2(s2[2], s2[3]));
+          l = (m > -INFINITY ? l * ex2(m - mn) : 0.f) + (st.x + st.y);
+          m = mn;
         }
         tc_fence_before();
         __syncwarp();
@@ -244,32 +263,39 @@ __global__ void __launch_bounds__(STC_THREADS, 2)
         mbar_wait(s_full + b, (i >> 1) & 1);
         tc_fence_after();
         float ca = 0.f, cbs = 0.f;
+        const float2 sc2 = make_float2(scale_log2, scale_log2);
 #pragma unroll
-        for (int c = 0; c < BLK / 32; ++c) {
-          // admitted rows of this 32-row chunk as a bit mask: [lo, L) of its slab, chunk-local
-          const int base = (c & 1) * 32;
-          const int lo = (c < 2 ? lo_a : lo_b) - base, hi = (c < 2 ? La : Lb) - base;
-          const int l0 = min(max(lo, 0), 32), h0 = min(max(hi, 0), 32);
-          const uint32_t mask = (h0 > l0) ? ((h0 == 32 ? 0xffffffffu : ((1u << h0) - 1u)) & ~((1u << l0) - 1u)) : 0u;
-          if (!__any_sync(0xffffffffu, mask != 0u)) continue;  // no admitted row in this chunk for the warp
-          uint32_t raw[32];
-          tmem_ld32(tmem + b * 128 + c * 32 + lane_off, raw);
+        for (int h = 0; h < 2; ++h) {  // rows of slab a (h = 0) / slab b (h = 1): 64 columns
+          const int lo = h ? lo_b : lo_a, hi = h ? Lb : La;  // admitted rows [lo, hi) of the slab
+          if (!__any_sync(0xffffffffu, hi > lo)) continue;  // no admitted row for the warp
+          uint32_t raw[2][32];
+          tmem_ld32(tmem + b * 128 + h * 64 + lane_off, raw[0]);
+          tmem_ld32(tmem + b * 128 + h * 64 + 32 + lane_off, raw[1]);
           tmem_wait_ld();
-          float acc = 0.f;
+          const bool all = __all_sync(0xffffffffu, lo == 0 && hi == 64);
+          float2 a2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-          for (int k4 = 0; k4 < 32; k4 += 4) {
-            const float4 M4 = *reinterpret_cast<const float4*>(Mr + c * 32 + k4);
-            const float Mk[4] = {M4.x, M4.y, M4.z, M4.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float v = ex2(__uint_as_float(raw[k4 + e]) * scale_log2 - Mk[e]);
-              acc += ((mask >> (k4 + e)) & 1u) ? v : 0.f;
+          for (int k = 0; k < 64; k += 4) {
+            const float4 M4 = *reinterpret_cast<const float4*>(Mr + h * 64 + k);
+            const float2 x0 = ffma2(make_float2(__uint_as_float(raw[k / 32][k % 32]), __uint_as_float(raw[k / 32][k % 32 + 1])),
+                                    sc2, make_float2(-M4.x, -M4.y));
+            const float2 x1 = ffma2(make_float2(__uint_as_float(raw[k / 32][k % 32 + 2]), __uint_as_float(raw[k / 32][k % 32 + 3])),
+                                    sc2, make_float2(-M4.z, -M4.w));
+            float2 e0 = make_float2(ex2(x0.x), ex2(x0.y)), e1 = make_float2(ex2(x1.x), ex2(x1.y));
+            if (!all) {
+              e0.x = (k >= lo && k < hi) ? e0.x : 0.f;
+              e0.y = (k + 1 >= lo && k + 1 < hi) ? e0.y : 0.f;
+              e1.x = (k + 2 >= lo && k + 2 < hi) ? e1.x : 0.f;
+              e1.y = (k + 3 >= lo && k + 3 < hi) ? e1.y : 0.f;
             }
+            a2[(k / 4) % 2] = fadd2(a2[(k / 4) % 2], e0);
+            a2[2 + (k / 4) % 2] = fadd2(a2[2 + (k / 4) % 2], e1);
           }
-          if (c < 2)
-            ca += acc;
+          const float2 t2 = fadd2(fadd2(a2[0], a2[1]), fadd2(a2[2], a2[3]));
+          if (h == 0)
+            ca = t2.x + t2.y;
           else
-            cbs += acc;
+            cbs = t2.x + t2.y;
         }
         tc_fence_before();
         __syncwarp();

@@ -1,6 +1,10 @@
 """Protocol model of attn_kernel's warp roles (csrc/attn.cu): the dynamic two-half MMA issuer state
 machine, the Q / K / V / key-coordinate loaders and the two softmax halves with their pv_done
-"owe" bookkeeping, run under random interleavings over random per-half tile-liveness patterns.
+bookkeeping, run under random interleavings over random per-half tile-liveness patterns.  The
+kernel's issuer ("static") uses pv_done[h] as a completion counter waited only by a rescale, with
+the parity of P V number n - 1 at sub-tile n -- the check below proves that wait unambiguous (at
+most one phase outstanding); the dropped "dynamic" issuer needed a per-slot barrier that every
+phase is waited on ("owe" bookkeeping).
 Every mbarrier is a phase counter; a wait on a phase that an unobserved later phase already
 overtook is reported as aliasing (the parity wait would be ambiguous), and a state where no role
 can move is a deadlock.  MMAs complete at issue (the protocol, not the timing, is modelled)."""
@@ -32,6 +36,7 @@ def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False):
     for h in range(2):
         bar(f"oe{h}"); bar(f"of{h}")
         for u in range(2): bar(f"sf{h}{u}"); bar(f"pf{h}{u}"); bar(f"pv{h}{u}")
+        bar(f"pv{h}")
     bar("qf"); bar("qe")
     live_s = [0] * KST
 
@@ -77,7 +82,7 @@ def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False):
                 if not (started >> h) & 1:
                     yield from wait(f"oe{h}", ocount[h] - 1)
                 started |= 1 << h
-                B[f"pv{h}{u}"].arrive()
+                B[f"pv{h}"].arrive()
             def issue_s(h):
                 B[f"sf{h}0"].arrive()  # one commit for both 64-key slots of the M128 N128 group
             g = None
@@ -95,19 +100,23 @@ def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False):
                 if ahead:
                     yield from wait(f"kf{ks}", kph_count[0] // KST); kph_count[0] += 1
                     live_next = live_s[ks]
-                for h in range(nh):
-                    if (live_cur >> h) & 1: yield from issue_pv(h, 0)
-                for h in range(nh):
-                    if (live_cur >> h) & 1: yield from issue_pv(h, 1)
-                    if ahead and (live_next >> h) & 1: issue_s(h)
+                if ahead:
+                    for h in range(nh):
+                        if (live_cur >> h) & 1: yield from issue_pv(h, 0)
+                    for h in range(nh):
+                        if (live_cur >> h) & 1: yield from issue_pv(h, 1)
+                        if (live_next >> h) & 1: issue_s(h)
+                else:
+                    for h in range(nh):
+                        if (live_cur >> h) & 1:
+                            yield from issue_pv(h, 0); yield from issue_pv(h, 1)
+                        if (started >> h) & 1:
+                            B[f"of{h}"].arrive(); ocount[h] += 1
                 if t + 1 == n - 1: B["qe"].arrive()
                 B[f"ve{vs}"].arrive(); vs = (vs + 1) % VST
                 if ahead:
                     B[f"ke{ks}"].arrive(); ks = (ks + 1) % KST
                 live_cur = live_next
-            for h in range(nh):
-                if (started >> h) & 1:
-                    B[f"of{h}"].arrive(); ocount[h] += 1
     kph_count = [0]; vph_count = [0]
     def issuer():
         kr_g = 0
@@ -216,7 +225,7 @@ def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False):
             kr_g = gb + n
     def softmax(h):
         kp = 0
-        sph = [0, 0]; pvph = [0, 0]; owe = [False, False]; oph = 0
+        sph = [0, 0]; pvph = [0, 0]; owe = [False, False]; oph = 0; nsub = 0
         for it in items:
             n = it["n"]
             present = h == 0 or it["has_b"]
@@ -230,6 +239,11 @@ def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False):
                 for u in range(2):
                     if issuer != "static" or u == 0:
                         yield from wait(f"sf{h}{u}", sph[u]); sph[u] += 1
+                    if issuer == "static":
+                        if rnd.random() < 0.3 and nsub > 0:  # rescale: P V number nsub - 1 landed
+                            yield from wait(f"pv{h}", nsub - 1)
+                        B[f"pf{h}{u}"].arrive(); nsub += 1
+                        continue
                     if owe[u]:
                         yield from wait(f"pv{h}{u}", pvph[u]); pvph[u] += 1; owe[u] = False
                     if rnd.random() < 0.3 and owe[u ^ 1]:
