@@ -19,6 +19,7 @@
 
 using namespace mmi;
 
+
 static thread_local char g_err[1024];
 static long long* g_dbg = nullptr;  // debug-only per-item timestamps (mmi_debug_set_timestamps)
 extern "C" MMI_API void mmi_debug_set_timestamps(long long* p) { g_dbg = p; }
@@ -112,7 +113,10 @@ static mmi_status get_plan(const mmi_problem* pb, const mmi_head_config* cfg, st
   if (need_blob && !out->blob_pinned) {
     const std::vector<uint8_t> blob = make_blob(out->P);
     uint8_t* pin = nullptr;
-    cudaError_t ce = cudaHostAlloc(reinterpret_cast<void**>(&pin), std::max<size_t>(blob.size(), 16), cudaHostAllocDefault);
+    // mapped: the estimate call's copy kernel reads it over PCIe (no copy-engine transfer, which
+    // would queue behind the caller's large host <-> device copies on other streams)
+    cudaError_t ce = cudaHostAlloc(reinterpret_cast<void**>(&pin), std::max<size_t>(blob.size(), 16),
+                                   cudaHostAllocMapped | cudaHostAllocPortable);
     if (ce != cudaSuccess) return fail(MMI_E_CUDA, "cudaHostAlloc(device tables): %s", cudaGetErrorString(ce));
     memcpy(pin, blob.data(), blob.size());
     ce = cudaEventCreateWithFlags(&out->last_upload, cudaEventDisableTiming);
@@ -241,17 +245,21 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
   if (!q || !k || !modality) return fail(MMI_E_INVALID, "null tensor pointer");
   cudaStream_t s = (cudaStream_t)stream;
   const int S = P.S;
-  // device tables: asynchronous copy from the plan's pinned host blob
-  CK(cudaMemcpyAsync(at<char>(ws, P.blob), cp->blob_pinned, P.blob_bytes, cudaMemcpyHostToDevice, s));
+  // device tables from the plan's pinned (mapped) host blob, and the labels: copy kernels, not
+  // copy-engine transfers -- a DMA copy on this stream would wait behind any large host <-> device
+  // copy the caller has queued on another stream (HostSparsePrefill's input copies)
+  void* blob_dev = nullptr;
+  CK(cudaHostGetDevicePointer(&blob_dev, cp->blob_pinned, 0));
+  CK(copy_bytes(at<char>(ws, P.blob), blob_dev, P.blob_bytes, s));
   CK(cudaEventRecord(cp->last_upload, s));
-  CK(cudaMemcpyAsync(at<uint8_t>(ws, P.labels), modality, S, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemsetAsync(at<char>(ws, P.flags), 0, P.flags.bytes, s));
+  CK(copy_bytes(at<uint8_t>(ws, P.labels), modality, (size_t)S, s));
+  CK(fill_bytes(at<char>(ws, P.flags), 0, P.flags.bytes, s));
   // zero the accumulators
-  CK(cudaMemsetAsync(at<char>(ws, P.cbuf), 0, P.cbuf.bytes, s));
-  CK(cudaMemsetAsync(at<char>(ws, P.dgbuf), 0, P.dgbuf.bytes, s));
-  CK(cudaMemsetAsync(at<char>(ws, P.bits), 0, P.bits.bytes, s));
-  CK(cudaMemsetAsync(at<char>(ws, P.vs_cnt), 0, P.vs_cnt.bytes, s));
-  CK(cudaMemsetAsync(at<char>(ws, P.seg_cnt), 0, P.seg_cnt.bytes, s));
+  CK(fill_bytes(at<char>(ws, P.cbuf), 0, P.cbuf.bytes, s));
+  CK(fill_bytes(at<char>(ws, P.dgbuf), 0, P.dgbuf.bytes, s));
+  CK(fill_bytes(at<char>(ws, P.bits), 0, P.bits.bytes, s));
+  CK(fill_bytes(at<char>(ws, P.vs_cnt), 0, P.vs_cnt.bytes, s));
+  CK(fill_bytes(at<char>(ws, P.seg_cnt), 0, P.seg_cnt.bytes, s));
   const int64_t mod_cap = (P.S + (int64_t)P.M * BLK + BLK - 1) / BLK * BLK;
   IndexCtx C = make_ctx(P, ws);
   int* info = at<int>(ws, P.mod_cnt);
@@ -352,7 +360,7 @@ static mmi_status run_sparse(const Plan& P, const mmi_problem* pb, void* ws, con
   // partial rows of work items without a live tile are never written: NaN-fill their LSEs so the
   // merges of mmi_unpermute skip them (0xFF bytes = NaN)
   if (P.part_rows > 0) {
-    const cudaError_t ce = cudaMemsetAsync(A.part_lse, 0xFF, sizeof(float) * (size_t)P.part_rows, s);
+    const cudaError_t ce = fill_bytes(A.part_lse, 0xFF, sizeof(float) * (size_t)P.part_rows, s);
     if (ce != cudaSuccess) return fail(MMI_E_CUDA, "partial LSE fill: %s", cudaGetErrorString(ce));
   }
   AttnLaunch L;

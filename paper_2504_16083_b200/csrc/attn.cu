@@ -1353,7 +1353,7 @@ cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hi
   if (grid <= 0) return cudaSuccess;
   const AttnParams& Pl = P;
   if (Pl.sched) {  // the caller's workspace counter, zeroed in stream order before the launch
-    const cudaError_t ce = cudaMemsetAsync(Pl.sched, 0, sizeof(unsigned int), stream);
+    const cudaError_t ce = fill_bytes(Pl.sched, 0, sizeof(unsigned int), stream);
     if (ce != cudaSuccess) return ce;
   }
   if (P.D == 128) {

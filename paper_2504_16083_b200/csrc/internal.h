@@ -130,4 +130,8 @@ struct AttnLaunch {
 cudaError_t launch_attn(const AttnLaunch& L, const AttnParams& P, int n_items_hint, cudaStream_t stream,
                         int* tmap_err);
 
+// kernel-based byte copy / fill (util.cu): never queued behind the caller's copy-engine transfers
+cudaError_t copy_bytes(void* dst, const void* src, size_t n, cudaStream_t s);
+cudaError_t fill_bytes(void* dst, uint8_t v, size_t n, cudaStream_t s);
+
 }  // namespace mmi

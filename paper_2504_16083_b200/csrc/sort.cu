@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "internal.h"
 #include "sort.h"
 
 namespace mmi {
@@ -188,8 +189,8 @@ void launch_sort_pairs(uint32_t* keys, uint32_t* keys_alt, int* vals, int* vals_
     int* tv = vi; vi = vo; vo = tv;
   }
   if (passes & 1) {  // result must end in keys / vals
-    cudaMemcpyAsync(keys, ki, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(vals, vi, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
+    copy_bytes(keys, ki, sizeof(uint32_t) * n, st);
+    copy_bytes(vals, vi, sizeof(int) * n, st);
   }
 }
 

@@ -266,18 +266,27 @@ def mmi_export_index(pb, cfgs, ws, head: int, stream=None) -> torch.Tensor:
 
 # ------------------------------------------------------------------ convenience
 class SparsePrefill:
-    """One layer's sparse pre-fill: owns the workspace and the marshalled C
-    structs; each call runs the four C-ABI calls on the current stream."""
+    """One layer's sparse pre-fill: owns the workspace (or uses a caller's buffer of at least
+    `workspace_bytes()`) and the marshalled C structs; each call runs the four C-ABI calls on the
+    current stream."""
 
-    def __init__(self, pb: Problem, cfgs: List[HeadConfig], device="cuda"):
+    def __init__(self, pb: Problem, cfgs: List[HeadConfig], device="cuda", ws: Optional[torch.Tensor] = None):
         self.pb, self.cfgs = pb, list(cfgs)
         self.c_pb = to_c_problem(pb)
         self.c_cfg = to_c_configs(self.cfgs)
+        nbytes = self.workspace_bytes()
+        if ws is None:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        elif ws.numel() * ws.element_size() < nbytes:
+            raise MMIError(5, "workspace buffer smaller than mmi_workspace_bytes")
+        self.ws = ws
+        self.ws_bytes = ws.numel() * ws.element_size()
+
+    def workspace_bytes(self) -> int:
         nbytes = int(lib().mmi_workspace_bytes(ctypes.byref(self.c_pb), self.c_cfg))
         if nbytes == 0:
             raise MMIError(1, lib().mmi_last_error().decode())
-        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        self.ws_bytes = nbytes
+        return nbytes
 
     def estimate(self, q, k, modality, stream=None):
         _need_cuda(q, k, modality)
@@ -343,31 +352,52 @@ class HostSparsePrefill:
     """End-to-end sparse pre-fill from pinned HOST buffers: each call copies the
     step's inputs host -> device, runs the four C-ABI calls and copies O back.
 
-    Heads are independent (Alg.1-3 act per head), so the layer is processed in
-    chunks of whole KV-head groups, one stream each: the host -> device copy of
-    chunk c + 1 and the device -> host copy of chunk c - 1 run while chunk c
-    computes (the copy engines are full duplex).  Every chunk
-    is the same library call on a sub-problem, so O is identical to the
-    one-shot call.  The caller's stream waits for every chunk before returning."""
+    Heads are independent (Alg.1-3 act per head), so the layer is processed in chunks of
+    heads (a KV group's K and V are copied once, before its first chunk).  Three streams: host -> device copies in chunk order, the chunks' library
+    calls in chunk order (one shared workspace), device -> host copies of each chunk's O --
+    chunk c computes while chunk c + 1 is copied in and chunk c - 1 copied out (the copy
+    engines are full duplex), so the step is bound by the input copy, not by its sum with the
+    compute.  Every chunk is the same library call on a sub-problem, so O is bit-identical to
+    the one-shot call.  The caller's stream waits for the last copy before returning."""
 
     def __init__(self, pb: Problem, cfgs: List[HeadConfig], device="cuda", n_chunks: Optional[int] = None):
         H, Hkv, S, D = pb.n_heads, pb.n_kv_heads, pb.seq_len, pb.head_dim
         G = H // Hkv
-        n = max(1, min(Hkv, n_chunks if n_chunks else 4))
+        # default: about 16K tokens of one head per chunk-head -- enough work per chunk to amortise
+        # the estimation launches, small enough that the last chunk's compute and output copy
+        # (the only parts not hidden under the input copy) are short (measured on one B200:
+        # 1M: 4 / 8 / 14 / 28 chunks -> 236 / 215 / 204 / 199 ms; 128K: 30.1 / 28.7 / 30.4 / 36.6 ms)
+        if not n_chunks:
+            n_chunks = min(H, max(Hkv, S // 16384))
+        n = max(1, min(H, n_chunks))
+        cfgs = list(cfgs)
         self.pb, self.chunks = pb, []
-        for c in range(n):
-            g0, g1 = c * Hkv // n, (c + 1) * Hkv // n
-            if g1 <= g0:
+        if n <= Hkv:  # whole KV groups per chunk
+            bounds = [(c * Hkv // n * G, (c + 1) * Hkv // n * G) for c in range(n)]
+        else:  # every group split into ceil(n / Hkv) head ranges
+            per = -(-n // Hkv)
+            bounds = [(g * G + i * G // per, g * G + (i + 1) * G // per) for g in range(Hkv) for i in range(per)]
+        sps = []
+        for h0, h1 in bounds:
+            if h1 <= h0:
                 continue
-            sub = Problem(G * (g1 - g0), g1 - g0, S, D, pb.n_modalities, pb.last_q, pb.block, pb.scale)
-            self.chunks.append(dict(h0=g0 * G, h1=g1 * G, g0=g0, g1=g1,
-                                    sp=SparsePrefill(sub, list(cfgs)[g0 * G:g1 * G], device)))
+            g0, g1 = h0 // G, (h1 - 1) // G + 1
+            sub = Problem(h1 - h0, g1 - g0, S, D, pb.n_modalities, pb.last_q, pb.block, pb.scale)
+            sp = SparsePrefill.__new__(SparsePrefill)
+            sp.pb, sp.cfgs = sub, cfgs[h0:h1]
+            sp.c_pb, sp.c_cfg = to_c_problem(sub), to_c_configs(sp.cfgs)
+            sps.append(sp)
+            self.chunks.append(dict(h0=h0, h1=h1, g0=g0, g1=g1, sp=sp))
+        # one workspace for every chunk: the chunks run in order on the compute stream
+        self.ws = torch.empty(max(sp.workspace_bytes() for sp in sps), dtype=torch.uint8, device=device)
+        for sp in sps:
+            sp.ws, sp.ws_bytes = self.ws, self.ws.numel()
         self.q = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
         self.k = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
         self.v = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
         self.lab = torch.empty((S,), dtype=torch.uint8, device=device)
         self.o = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
-        self.streams = [torch.cuda.Stream(device=device) for _ in self.chunks]
+        self.s_in, self.s_cmp, self.s_out = (torch.cuda.Stream(device=device) for _ in range(3))
 
     def h2d_bytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in (self.q, self.k, self.v, self.lab))
@@ -379,26 +409,33 @@ class HostSparsePrefill:
         caller = stream if stream is not None else torch.cuda.current_stream()
         start = torch.cuda.Event()
         start.record(caller)
-        for st in self.streams:
+        for st in (self.s_in, self.s_cmp, self.s_out):
             st.wait_event(start)
-        with torch.cuda.stream(self.streams[0]):
+        kv_done = -1  # K / V of groups < kv_done are on the device
+        with torch.cuda.stream(self.s_in):
             self.lab.copy_(lab_h, non_blocking=True)
-            lab_ready = torch.cuda.Event()
-            lab_ready.record(self.streams[0])
-        for i, ch in enumerate(self.chunks):
-            st = self.streams[i % len(self.streams)]
-            st.wait_event(lab_ready)
+        for ch in self.chunks:
             h0, h1, g0, g1 = ch["h0"], ch["h1"], ch["g0"], ch["g1"]
-            with torch.cuda.stream(st):
+            with torch.cuda.stream(self.s_in):
+                if g1 > kv_done:
+                    a = max(g0, kv_done)
+                    self.k[a:g1].copy_(k_h[a:g1], non_blocking=True)
+                    self.v[a:g1].copy_(v_h[a:g1], non_blocking=True)
+                    kv_done = g1
                 self.q[h0:h1].copy_(q_h[h0:h1], non_blocking=True)
-                self.k[g0:g1].copy_(k_h[g0:g1], non_blocking=True)
-                self.v[g0:g1].copy_(v_h[g0:g1], non_blocking=True)
-                ch["sp"](self.q[h0:h1], self.k[g0:g1], self.v[g0:g1], self.lab, o=self.o[h0:h1], stream=st)
+                ready = torch.cuda.Event()
+                ready.record(self.s_in)
+            self.s_cmp.wait_event(ready)
+            with torch.cuda.stream(self.s_cmp):
+                ch["sp"](self.q[h0:h1], self.k[g0:g1], self.v[g0:g1], self.lab, o=self.o[h0:h1], stream=self.s_cmp)
+                computed = torch.cuda.Event()
+                computed.record(self.s_cmp)
+            self.s_out.wait_event(computed)
+            with torch.cuda.stream(self.s_out):
                 o_h[h0:h1].copy_(self.o[h0:h1], non_blocking=True)
-        for st in self.streams:
-            done = torch.cuda.Event()
-            done.record(st)
-            caller.wait_event(done)
+        done = torch.cuda.Event()
+        done.record(self.s_out)
+        caller.wait_event(done)
         return o_h
 
 

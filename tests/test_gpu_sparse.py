@@ -84,10 +84,11 @@ def test_determinism():
     assert torch.equal(a["lse"], b["lse"])
 
 
-@pytest.mark.parametrize("n_chunks", [1, 2, 4])
+@pytest.mark.parametrize("n_chunks", [1, 2, 4, 8])
 def test_host_pipeline_matches_device_call(n_chunks):
-    """The end-to-end host path (KV-group chunks on their own streams, copies overlapped with
-    compute) gives the bit-identical O of one device-resident call: heads are independent."""
+    """The end-to-end host path (chunks of KV groups or of single heads, input copies / compute /
+    output copies on three streams) gives the bit-identical O of one device-resident call: heads
+    are independent."""
     import paper_2504_16083_b200 as mmi
     heads = _mixed_no_boundary_heads()[:8]
     wl = small_workload(S_frames=12, text=100, H=8, Hkv=4, D=128, heads=heads)
