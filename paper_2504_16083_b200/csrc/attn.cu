@@ -586,6 +586,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         constexpr bool leader = true;
 #endif
         constexpr uint32_t IDESC_S128 = idesc_bf16(128, 128, 0);
+        [[maybe_unused]] constexpr uint32_t IDESC_S64 = idesc_bf16(128, 64, 0);
         constexpr uint32_t IDESC_O = idesc_bf16(128, D, 1);
         const uint32_t q_base = smem_u32(smem + L::OFF_Q);
         const uint32_t k_base = smem_u32(smem + L::OFF_K);
@@ -654,13 +655,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             if (leader) umma_commit(s_full + 2 * hf);  // both 64-key slots: one phase per tile
           };
+#ifdef MMI_S64
+          // (experiment) S of one 64-key slot, issued right after the P V that freed the slot
+          auto issue_s64 = [&](int hf, int kst, int u) {
+            TR(2, 2 * hf + u);
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (k / 4) * (BLK * 128) + (k % 4) * 32;
+              const uint64_t ad = dq0 + (uint64_t)((hf * L::Q_BYTES + off) >> 4);
+              const uint64_t bd = dk0 + (uint64_t)((kst * L::KV_BYTES + u * 64 * 128 + off) >> 4);
+              if (leader) umma_ss(tmem + 128 * hf + 64 * u, ad, bd, IDESC_S64, k > 0 ? 1u : 0u);
+            }
+            if (leader) umma_commit(s_full + 2 * hf + u);
+          };
+#endif
           t0 = PROF_T();
           mbar_wait(k_full + ks, k_phase);
           PROF_ADD(wk, t0);
           tc_fence_after();
           uint32_t live_cur = (uint32_t)live_s[ks], live_next = 0;
           for (int hf = 0; hf < nh; ++hf)
-            if ((live_cur >> hf) & 1u) issue_s128(hf, ks);
+            if ((live_cur >> hf) & 1u) {
+#ifdef MMI_S64
+              issue_s64(hf, ks, 0);
+              issue_s64(hf, ks, 1);
+#else
+              issue_s128(hf, ks);
+#endif
+            }
           if (n == 1 && leader) umma_commit(q_empty);  // last S of the item issued
           if (leader) umma_commit(k_empty + ks);
           if (++ks == KST) {
@@ -683,12 +705,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             prof_nt += 2 * nh;
 #endif
             if (ahead) {
+#ifdef MMI_S64
+              for (int u = 0; u < 2; ++u)
+                for (int hf = 0; hf < nh; ++hf) {
+                  if ((live_cur >> hf) & 1u) issue_pv(hf, 2 * t + u);
+                  if ((live_next >> hf) & 1u) issue_s64(hf, ks, u);
+                }
+#else
               for (int hf = 0; hf < nh; ++hf)
                 if ((live_cur >> hf) & 1u) issue_pv(hf, 2 * t);
               for (int hf = 0; hf < nh; ++hf) {
                 if ((live_cur >> hf) & 1u) issue_pv(hf, 2 * t + 1);
                 if ((live_next >> hf) & 1u) issue_s128(hf, ks);
               }
+#endif
             } else {
               // last tile: each half's P V pair, then its O is complete -- half A's epilogue does
               // not wait for half B's last softmax
@@ -954,10 +984,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             t0 = PROF_T();
+#ifdef MMI_S64
+            mbar_wait(s_full + 2 * hf + u, (s_phase[j] >> u) & 1u);  // per-slot S
+            s_phase[j] ^= 1u << u;
+#else
             if (u == 0) {  // S of both 64-key slots landed together (one M128 N128 group)
               mbar_wait(s_full + 2 * hf, s_phase[j]);
               s_phase[j] ^= 1;
             }
+#endif
             PROF_ADD(sws, t0);
             TR(4, u);
             t0 = PROF_T();
@@ -1149,7 +1184,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         const uint32_t ebuf = smem_u32(smem + L::OFF_EPI + (warp - NWARP_CTRL) * 32 * EPI_STRIDE);
         const int wrow0 = (warp % 4) * 32;  // first row of this warp in the half (its TMEM lane base)
-#ifdef MMI_EPI_NOTMA
+#if defined(MMI_EPI_NOTMA)
         if (false) {
 #else
         if (!fin || (!it.q_gathered && __all_sync(0xffffffffu, write[j]))) {

@@ -104,5 +104,5 @@ for tool in ("memcheck", "racecheck", "synccheck", "initcheck"):
         summ = [l for l in t if "ERROR SUMMARY" in l or l.startswith("tool=") or "sanitize run ok" in l
                 or "Barrier error" in l][:6]
         out.append(f"\ncompute-sanitizer {tool}: " + " / ".join(summ))
-open("profiles/r2_summary.md", "w").write("\n".join(out) + "\n")
+open(sys.argv[2] if len(sys.argv) > 2 else "profiles/r2_summary.md", "w").write("\n".join(out) + "\n")
 print("\n".join(out[:40]))

@@ -20,11 +20,12 @@ class Bar:
     def check(s, k):
         if s.done > k + 1: raise RuntimeError(f"aliasing on {s.name}: waiting phase {k}, done {s.done}")
 
-def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False):
+def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False, s64=False):
     """issuer="static": the kernel's issuer (per key tile P_A(t,0)V P_B(t,0)V P_A(t,1)V S_A(t+1)
     P_B(t,1)V S_B(t+1)); "dynamic": the measured-and-dropped per-half dynamic issuer (N=64 scores
     one tile ahead); coupled=True with "dynamic": its first version, whose state 2 blocked on the
-    next tile's K load (deadlocks)."""
+    next tile's K load (deadlocks); s64=True with "static": S as two N=64 slot groups, each issued
+    right after the P V that freed its slot (MMI_S64)."""
     rnd = random.Random(seed)
     B = {}
     def bar(n, c=1):
@@ -83,8 +84,11 @@ def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False):
                     yield from wait(f"oe{h}", ocount[h] - 1)
                 started |= 1 << h
                 B[f"pv{h}"].arrive()
-            def issue_s(h):
-                B[f"sf{h}0"].arrive()  # one commit for both 64-key slots of the M128 N128 group
+            def issue_s(h, u=None):
+                if not s64:
+                    B[f"sf{h}0"].arrive()  # one commit for both 64-key slots of the M128 N128 group
+                else:
+                    for x in ((0, 1) if u is None else (u,)): B[f"sf{h}{x}"].arrive()
             g = None
             yield from wait(f"kf{ks}", kph_count[0] // KST)
             kph_count[0] += 1
@@ -100,7 +104,12 @@ def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False):
                 if ahead:
                     yield from wait(f"kf{ks}", kph_count[0] // KST); kph_count[0] += 1
                     live_next = live_s[ks]
-                if ahead:
+                if ahead and s64:
+                    for u in range(2):
+                        for h in range(nh):
+                            if (live_cur >> h) & 1: yield from issue_pv(h, u)
+                            if (live_next >> h) & 1: issue_s(h, u)
+                elif ahead:
                     for h in range(nh):
                         if (live_cur >> h) & 1: yield from issue_pv(h, 0)
                     for h in range(nh):
@@ -237,7 +246,7 @@ def run(items, KST=2, VST=2, NKP=4, seed=0, issuer="static", coupled=False):
                 if not present or not (it["live"][t] >> h) & 1: continue
                 nl += 1
                 for u in range(2):
-                    if issuer != "static" or u == 0:
+                    if issuer != "static" or u == 0 or s64:
                         yield from wait(f"sf{h}{u}", sph[u]); sph[u] += 1
                     if issuer == "static":
                         if rnd.random() < 0.3 and nsub > 0:  # rescale: P V number nsub - 1 landed

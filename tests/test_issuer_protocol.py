@@ -9,12 +9,13 @@ import issuer_sim
 
 
 @pytest.mark.parametrize("kst", [2, 3])
-@pytest.mark.parametrize("issuer", ["static", "dynamic"])
+@pytest.mark.parametrize("issuer", ["static", "static-s64", "dynamic"])
 def test_issuer_protocol_random(kst, issuer):
     rnd = random.Random(100 + kst)
     for trial in range(200):
         items = issuer_sim.rand_items(rnd, rnd.randint(1, 6))
-        r, state, alive = issuer_sim.run(items, KST=kst, VST=kst, seed=trial, issuer=issuer)
+        r, state, alive = issuer_sim.run(items, KST=kst, VST=kst, seed=trial, issuer=issuer.split("-")[0],
+                                         s64=issuer.endswith("s64"))
         assert r == "ok", (trial, items, alive, state)
 
 
