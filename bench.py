@@ -566,7 +566,9 @@ def main():
             v_h = d["v"][kv0:kv1].contiguous().pin_memory()
             lab_h = torch.from_numpy(np.ascontiguousarray(d["labels"])).pin_memory()
             o_h = torch.empty(q_h.shape, dtype=torch.bfloat16).pin_memory()
-            for _ in range(max(1, args.warmup // 2)):
+            # warm-up: the first call also picks the chunking (HostSparsePrefill), the second
+            # builds the chosen chunks' plans
+            for _ in range(max(2, args.warmup // 2)):
                 hp(q_h, k_h, v_h, lab_h, o_h)
             torch.cuda.synchronize()
             if dist: dist.barrier()

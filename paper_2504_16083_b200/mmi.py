@@ -353,31 +353,46 @@ class HostSparsePrefill:
     step's inputs host -> device, runs the four C-ABI calls and copies O back.
 
     Heads are independent (Alg.1-3 act per head), so the layer is processed in chunks of
-    heads (a KV group's K and V are copied once, before its first chunk).  Three streams: host -> device copies in chunk order, the chunks' library
-    calls in chunk order (one shared workspace), device -> host copies of each chunk's O --
-    chunk c computes while chunk c + 1 is copied in and chunk c - 1 copied out (the copy
-    engines are full duplex), so the step is bound by the input copy, not by its sum with the
-    compute.  Every chunk is the same library call on a sub-problem, so O is bit-identical to
-    the one-shot call.  The caller's stream waits for the last copy before returning."""
+    heads (a KV group's K and V are copied once, before its first chunk).  Three streams:
+    host -> device copies in chunk order, the chunks' library calls in chunk order (one shared
+    workspace), device -> host copies of each chunk's O -- chunk c computes while chunk c + 1 is
+    copied in and chunk c - 1 copied out (the copy engines are full duplex).  Every chunk is the
+    same library call on a sub-problem, so O is bit-identical to the one-shot call.  The
+    caller's stream waits for the last copy before returning.
+
+    Chunking: with n_chunks=None the first call runs one chunk per KV group and times its
+    compute against its input copy; a copy-bound layer then switches to chunks of about 16K
+    tokens x heads (the last chunk's compute and output copy, the only parts not hidden under
+    the input copy, get short), a compute-bound one keeps whole groups (fewer, longer kernels).
+    Measured on one B200 (ms/layer): 1M 4 / 8 / 14 / 28 chunks 236 / 215 / 204 / 199;
+    128K 30.1 / 28.7 / 30.4 / 36.6; 256K 229 / 238 / 268 / 255; 512K 257 / 263 / 313 / 382."""
+
+    TOKENS_PER_CHUNK = 16384  # fine chunking: about this many tokens x heads per chunk
 
     def __init__(self, pb: Problem, cfgs: List[HeadConfig], device="cuda", n_chunks: Optional[int] = None):
         H, Hkv, S, D = pb.n_heads, pb.n_kv_heads, pb.seq_len, pb.head_dim
+        self.pb, self.cfgs, self.device = pb, list(cfgs), device
+        self.ws = None
+        self.fixed = n_chunks is not None
+        self.chunks = self._build(max(1, min(H, n_chunks)) if n_chunks else Hkv)
+        self.fine = min(H, max(Hkv, S // self.TOKENS_PER_CHUNK))
+        self.q = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
+        self.k = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
+        self.v = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
+        self.lab = torch.empty((S,), dtype=torch.uint8, device=device)
+        self.o = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
+        self.s_in, self.s_cmp, self.s_out = (torch.cuda.Stream(device=device) for _ in range(3))
+
+    def _build(self, n: int):
+        pb, cfgs = self.pb, self.cfgs
+        H, Hkv, S, D = pb.n_heads, pb.n_kv_heads, pb.seq_len, pb.head_dim
         G = H // Hkv
-        # default: about 16K tokens of one head per chunk-head -- enough work per chunk to amortise
-        # the estimation launches, small enough that the last chunk's compute and output copy
-        # (the only parts not hidden under the input copy) are short (measured on one B200:
-        # 1M: 4 / 8 / 14 / 28 chunks -> 236 / 215 / 204 / 199 ms; 128K: 30.1 / 28.7 / 30.4 / 36.6 ms)
-        if not n_chunks:
-            n_chunks = min(H, max(Hkv, S // 16384))
-        n = max(1, min(H, n_chunks))
-        cfgs = list(cfgs)
-        self.pb, self.chunks = pb, []
         if n <= Hkv:  # whole KV groups per chunk
             bounds = [(c * Hkv // n * G, (c + 1) * Hkv // n * G) for c in range(n)]
         else:  # every group split into ceil(n / Hkv) head ranges
             per = -(-n // Hkv)
             bounds = [(g * G + i * G // per, g * G + (i + 1) * G // per) for g in range(Hkv) for i in range(per)]
-        sps = []
+        chunks = []
         for h0, h1 in bounds:
             if h1 <= h0:
                 continue
@@ -386,18 +401,16 @@ class HostSparsePrefill:
             sp = SparsePrefill.__new__(SparsePrefill)
             sp.pb, sp.cfgs = sub, cfgs[h0:h1]
             sp.c_pb, sp.c_cfg = to_c_problem(sub), to_c_configs(sp.cfgs)
-            sps.append(sp)
-            self.chunks.append(dict(h0=h0, h1=h1, g0=g0, g1=g1, sp=sp))
+            chunks.append(dict(h0=h0, h1=h1, g0=g0, g1=g1, sp=sp))
         # one workspace for every chunk: the chunks run in order on the compute stream
-        self.ws = torch.empty(max(sp.workspace_bytes() for sp in sps), dtype=torch.uint8, device=device)
-        for sp in sps:
-            sp.ws, sp.ws_bytes = self.ws, self.ws.numel()
-        self.q = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
-        self.k = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
-        self.v = torch.empty((Hkv, S, D), dtype=torch.bfloat16, device=device)
-        self.lab = torch.empty((S,), dtype=torch.uint8, device=device)
-        self.o = torch.empty((H, S, D), dtype=torch.bfloat16, device=device)
-        self.s_in, self.s_cmp, self.s_out = (torch.cuda.Stream(device=device) for _ in range(3))
+        need = max(ch["sp"].workspace_bytes() for ch in chunks)
+        if self.ws is None or self.ws.numel() < need:
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        for ch in chunks:
+            ch["sp"].ws, ch["sp"].ws_bytes = self.ws, self.ws.numel()
+        for ch in getattr(self, "chunks", []):  # earlier chunking shares the (possibly new) buffer
+            ch["sp"].ws, ch["sp"].ws_bytes = self.ws, self.ws.numel()
+        return chunks
 
     def h2d_bytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in (self.q, self.k, self.v, self.lab))
@@ -407,11 +420,14 @@ class HostSparsePrefill:
 
     def __call__(self, q_h, k_h, v_h, lab_h, o_h, stream=None):
         caller = stream if stream is not None else torch.cuda.current_stream()
-        start = torch.cuda.Event()
+        decide = not self.fixed and len(self.chunks) != self.fine
+        timing = decide and not getattr(self, "_decided", False)
+        start = torch.cuda.Event(enable_timing=timing)
         start.record(caller)
         for st in (self.s_in, self.s_cmp, self.s_out):
             st.wait_event(start)
         kv_done = -1  # K / V of groups < kv_done are on the device
+        marks = []
         with torch.cuda.stream(self.s_in):
             self.lab.copy_(lab_h, non_blocking=True)
         for ch in self.chunks:
@@ -423,19 +439,29 @@ class HostSparsePrefill:
                     self.v[a:g1].copy_(v_h[a:g1], non_blocking=True)
                     kv_done = g1
                 self.q[h0:h1].copy_(q_h[h0:h1], non_blocking=True)
-                ready = torch.cuda.Event()
+                ready = torch.cuda.Event(enable_timing=timing)
                 ready.record(self.s_in)
             self.s_cmp.wait_event(ready)
             with torch.cuda.stream(self.s_cmp):
+                c0 = torch.cuda.Event(enable_timing=timing)
+                c0.record(self.s_cmp)
                 ch["sp"](self.q[h0:h1], self.k[g0:g1], self.v[g0:g1], self.lab, o=self.o[h0:h1], stream=self.s_cmp)
-                computed = torch.cuda.Event()
+                computed = torch.cuda.Event(enable_timing=timing)
                 computed.record(self.s_cmp)
+            marks.append((ready, c0, computed))
             self.s_out.wait_event(computed)
             with torch.cuda.stream(self.s_out):
                 o_h[h0:h1].copy_(self.o[h0:h1], non_blocking=True)
         done = torch.cuda.Event()
         done.record(self.s_out)
         caller.wait_event(done)
+        if timing:  # first call: copy-bound -> fine chunks (synchronises once)
+            done.synchronize()
+            copy_ms = start.elapsed_time(marks[-1][0])
+            compute_ms = sum(c0.elapsed_time(c1) for _, c0, c1 in marks)
+            self._decided = True
+            if compute_ms < 0.6 * copy_ms:
+                self.chunks = self._build(self.fine)
         return o_h
 
 

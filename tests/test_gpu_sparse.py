@@ -107,6 +107,31 @@ def test_host_pipeline_matches_device_call(n_chunks):
         assert torch.equal(o_h, ref.cpu())
 
 
+def test_host_pipeline_adaptive_chunking():
+    """Default chunking: the first call runs KV-group chunks and times compute against the input
+    copy; a copy-bound layer switches to finer chunks.  O stays bit-identical across the switch."""
+    import paper_2504_16083_b200 as mmi
+    heads = _mixed_no_boundary_heads()[:8]
+    wl = small_workload(S_frames=12, text=100, H=8, Hkv=4, D=128, heads=heads)
+    d = gen_qkv(wl, seed=8)
+    pb = wl.problem
+    q, k, v = d["q"].cuda(), d["k"].cuda(), d["v"].cuda()
+    lab = torch.from_numpy(np.ascontiguousarray(d["labels"])).cuda()
+    ref = mmi.SparsePrefill(pb, wl.heads)(q, k, v, lab).cpu()
+    hp = mmi.HostSparsePrefill(pb, wl.heads)
+    hp.fine = pb.n_heads  # what a long layer would use: one head per chunk
+    n0 = len(hp.chunks)
+    args = (d["q"].contiguous().pin_memory(), d["k"].contiguous().pin_memory(), d["v"].contiguous().pin_memory(),
+            torch.from_numpy(np.ascontiguousarray(d["labels"])).pin_memory())
+    o_h = torch.empty(d["q"].shape, dtype=torch.bfloat16).pin_memory()
+    for _ in range(3):
+        o_h.zero_()
+        hp(*args, o_h)
+        torch.cuda.synchronize()
+        assert torch.equal(o_h, ref)
+    assert n0 == pb.n_kv_heads and len(hp.chunks) in (pb.n_kv_heads, pb.n_heads)
+
+
 @pytest.mark.parametrize("frames,text", [(0, 1), (0, 50), (0, 127), (0, 129), (1, 44)])
 def test_short_sequences(frames, text):
     """Degenerate lengths (S = 2 ... 344: a single partial tile, no grid window, fewer rows than
