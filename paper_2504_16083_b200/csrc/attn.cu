@@ -938,8 +938,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               range_mask(mw[j], n_sink, min(n_lt_local, n_causal) - 1);
             } else {
               // vertical-slash: coordinates contiguous in the tile (original K, or a modality's
-              // rank-ordered keys); slash bits of offsets x - ybase - c, bit-reversed window
-              range_mask(mw[j], 0, n_causal - 1);
+              // rank-ordered keys); slash bits of offsets x - ybase - c, bit-reversed window.  A
+              // slash range's first tile may start below key 0 (ybase < 0): those keys are masked.
+              range_mask(mw[j], -ybase, n_causal - 1);
               uint32_t ws[4], wv[4];
               bit_window(c_sl, x - ybase - (BLK - 1), ws);
               bit_window(c_vm, ybase, wv);

@@ -332,6 +332,7 @@ struct KView {
   int kind;          // 0 ORIG K, 1 MOD region (rank coords), 2 class view (CLS / one RES class), 3 VCOL
   int space;
   int row0;          // K-space row of tile 0
+  int base;          // ORIG: key position of index 0 (slash ranges start anywhere, even below 0)
   int n;             // valid keys
   int kv_base;       // ORIG: kv*S
   // class views
@@ -340,14 +341,14 @@ struct KView {
   const int* list;         // VCOL coords
   int list_rank;           // VCOL coords are ranks (use pos_of_rank)
   __device__ __forceinline__ int coord_at(int i) const {
-    if (kind == 0) return i;
+    if (kind == 0) return base + i;
     if (kind == 1) return i;
     if (kind == 2) return cls_r + cls_s * i;
     return list[i];
   }
   __device__ __forceinline__ int pos_at(int i) const {
     const int c = coord_at(i);
-    if (kind == 0) return c;
+    if (kind == 0) return c;  // (may be < 0 for a slash range: such keys are masked)
     if (kind == 1) return pos_of_rank[c];
     if (kind == 2) return pos_of_rank ? pos_of_rank[c] : c;
     return list_rank ? pos_of_rank[c] : c;
@@ -356,7 +357,8 @@ struct KView {
 
 // state of tile t of a K-view for the rows of one half (rows info R; `exists` false for an absent half)
 __device__ __forceinline__ uint32_t tile_state(const KView& kv, int t, uint32_t role, int rmode, const RowsInfo& R,
-                                               bool exists, int sink, int local) {
+                                               bool exists, int sink, int local, const int* sl = nullptr,
+                                               int ns = 0) {
   if (!exists) return TS_DEAD;
   const int i0 = t * BLK, i1 = min(t * BLK + BLK - 1, kv.n - 1);
   const int yp_lo = kv.pos_at(i0), yp_hi = kv.pos_at(i1);
@@ -368,6 +370,13 @@ __device__ __forceinline__ uint32_t tile_state(const KView& kv, int t, uint32_t 
   // the A part of a row x is y < sink or y > thr(x) (thr nondecreasing in x; a_thr, internal.h)
   if (role == R_A && y_lo >= sink && y_hi <= a_thr(x_lo, local)) return TS_DEAD;   // neither sink nor band
   if (role == R_NOTA && (y_hi < sink || y_lo > a_thr(x_hi, local))) return TS_DEAD;  // all inside the A part
+  if (role == R_VSSL && sl) {
+    // slash tile: live for the half iff some slash offset o = x - y joins one of its rows to one of
+    // the tile's keys (the index keeps the offsets ascending)
+    const int o_lo = max(x_lo - y_hi, 0), o_hi = x_hi - y_lo;
+    const int q = lower_bound_i(sl, ns, o_lo);
+    if (q >= ns || sl[q] > o_hi) return TS_DEAD;
+  }
   const bool pads = (t * BLK + BLK - 1 >= kv.n);
   if (pads || yp_hi > R.xp_lo) return TS_PRED;  // pad keys / not causally full
   if (role == R_TRUE) return TS_FULL;
@@ -378,14 +387,15 @@ __device__ __forceinline__ uint32_t tile_state(const KView& kv, int t, uint32_t 
 
 // emit tiles [t0, t1) of a K-view (segments of per-half DEAD / PRED / FULL runs)
 __device__ void emit_range(Emitter& E, const KView& kv, int t0, int t1, uint32_t role, int rmode, uint32_t inst,
-                           const RowsInfo (&RH)[2], int nh, int sink, int local) {
+                           const RowsInfo (&RH)[2], int nh, int sink, int local, const int* sl = nullptr,
+                           int ns = 0) {
   SegBuilder b;
   b.open = false;
   b.krow_t0 = kv.row0;
   b.meta = seg_meta(kv.space, role, rmode, inst);
   for (int t = t0; t < t1; ++t)
-    b.push(E, t, tile_state(kv, t, role, rmode, RH[0], true, sink, local),
-           tile_state(kv, t, role, rmode, RH[1], nh > 1, sink, local));
+    b.push(E, t, tile_state(kv, t, role, rmode, RH[0], true, sink, local, sl, ns),
+           tile_state(kv, t, role, rmode, RH[1], nh > 1, sink, local, sl, ns));
   b.flush(E);
 }
 
@@ -434,6 +444,7 @@ struct ItemCtx {
 // K-view of the pattern's key base (No/Q: original K; 2D: modality region kb)
 __device__ KView base_kview(const IndexCtx& C, const ItemCtx& I, const DInst& x) {
   KView k;
+  k.base = 0;
   k.cls_r = 0;
   k.cls_s = 1;
   k.list = nullptr;
@@ -492,6 +503,7 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
     if (x.kind == MMI_PAT_GRID && (x.flags & GF_V)) {
       const GridRes g = C.gridres[x.grid_id];
       KView kc;
+      kc.base = 0;
       kc.kind = 2;
       kc.space = 1;
       kc.row0 = kview_row0(C, x.v_cls_k);
@@ -511,6 +523,7 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
   if (x.kind == MMI_PAT_VSLASH) {
     const DView vv = C.views[x.v_vcol];
     KView kc;
+    kc.base = 0;
     kc.kind = 3;
     kc.space = 1;
     kc.row0 = vv.row_off;
@@ -527,30 +540,65 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
       emit_range(E, kc, 0, t1, R_TRUE, rmode, ii, RW.H, RW.nh, 0, 0);
     }
     if (!cross_pos) {
-      // slash offsets: key coords [x_lo - o, x_hi - o]; ranges move left as o grows
+      // slash offsets: key coords [x_lo - o, x_hi - o]; the windows move left as o grows
       const int ns = C.vs_cnt[x.vs_id * 2 + 1];
       const int* sl = C.vs_lists + C.vs_list_off[x.vs_id * 2 + 1];
-      int cl = 0, ch = -1;
-      for (int q = 0; q < ns; ++q) {
-        const int o = sl[q];
-        const int c_hi = x_hi - o;
-        if (c_hi < 0) break;
-        const int c_lo = max(0, x_lo - o);
-        int t0, t1;
-        coord_tiles(kb, c_lo, c_hi, t0, t1);
-        if (t1 <= t0) continue;
-        if (ch < cl) {
-          cl = t0;
-          ch = t1 - 1;
-        } else if (t1 - 1 >= cl - 1) {
-          cl = min(cl, t0);
-        } else {
-          emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0);
-          cl = t0;
-          ch = t1 - 1;
+      if (kb.kind == 0) {
+        // original K: tiles are anchored at the right end of each merged window range, so an
+        // isolated offset costs one tile per half (its window, exactly) instead of two or three
+        // 128-aligned tiles; a range's leftmost tile may start below key 0 (those keys are masked).
+        // Ranges are disjoint: a window that reaches into the current range's tile span joins it.
+        int rh = 0, rl = 0;
+        bool have = false;
+        auto flush = [&]() {
+          const int nt = (rh - rl + BLK) / BLK;
+          KView kt = kb;
+          kt.base = rh - nt * BLK + 1;
+          kt.row0 = kb.row0 + kt.base;
+          kt.n = kb.n - kt.base;
+          emit_range(E, kt, 0, nt, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0, sl, ns);
+        };
+        for (int q = 0; q < ns; ++q) {
+          const int o = sl[q];
+          const int wh = x_hi - o;
+          if (wh < 0) break;
+          const int wl = x_lo - o;
+          if (have) {
+            const int tl = rh - ((rh - rl + BLK) / BLK) * BLK + 1;  // current leftmost tile start
+            if (wh >= tl - 1) {
+              rl = min(rl, wl);
+              continue;
+            }
+            flush();
+          }
+          rh = wh;
+          rl = wl;
+          have = true;
         }
+        if (have) flush();
+      } else {
+        int cl = 0, ch = -1;
+        for (int q = 0; q < ns; ++q) {
+          const int o = sl[q];
+          const int c_hi = x_hi - o;
+          if (c_hi < 0) break;
+          const int c_lo = max(0, x_lo - o);
+          int t0, t1;
+          coord_tiles(kb, c_lo, c_hi, t0, t1);
+          if (t1 <= t0) continue;
+          if (ch < cl) {
+            cl = t0;
+            ch = t1 - 1;
+          } else if (t1 - 1 >= cl - 1) {
+            cl = min(cl, t0);
+          } else {
+            emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0, sl, ns);
+            cl = t0;
+            ch = t1 - 1;
+          }
+        }
+        if (ch >= cl) emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0, sl, ns);
       }
-      if (ch >= cl) emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0);
     }
     return;
   }
@@ -762,6 +810,7 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W,
       ClassGeo cg;
       cg.init(n, g.s);
       KView kc;
+      kc.base = 0;
       kc.kind = 2;
       kc.space = 1;
       kc.row0 = kview_row0(C, x.v_res_k) + cg.classoff(r);
