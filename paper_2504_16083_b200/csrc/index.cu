@@ -548,7 +548,7 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
         // isolated offset costs one tile per half (its window, exactly) instead of two or three
         // 128-aligned tiles; a range's leftmost tile may start below key 0 (those keys are masked).
         // Ranges are disjoint: a window that reaches into the current range's tile span joins it.
-        int rh = 0, rl = 0;
+        int rh = 0, rl = 0, qs = 0, qe = 0;  // current range: coords [rl, rh], offsets sl[qs..qe]
         bool have = false;
         auto flush = [&]() {
           const int nt = (rh - rl + BLK) / BLK;
@@ -556,7 +556,8 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
           kt.base = rh - nt * BLK + 1;
           kt.row0 = kb.row0 + kt.base;
           kt.n = kb.n - kt.base;
-          emit_range(E, kt, 0, nt, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0, sl, ns);
+          // the per-half states only need the range's own offsets (a short list)
+          emit_range(E, kt, 0, nt, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0, sl + qs, qe - qs + 1);
         };
         for (int q = 0; q < ns; ++q) {
           const int o = sl[q];
@@ -567,17 +568,19 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
             const int tl = rh - ((rh - rl + BLK) / BLK) * BLK + 1;  // current leftmost tile start
             if (wh >= tl - 1) {
               rl = min(rl, wl);
+              qe = q;
               continue;
             }
             flush();
           }
           rh = wh;
           rl = wl;
+          qs = qe = q;
           have = true;
         }
         if (have) flush();
       } else {
-        int cl = 0, ch = -1;
+        int cl = 0, ch = -1, qs = 0, qe = -1;
         for (int q = 0; q < ns; ++q) {
           const int o = sl[q];
           const int c_hi = x_hi - o;
@@ -589,15 +592,18 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
           if (ch < cl) {
             cl = t0;
             ch = t1 - 1;
+            qs = qe = q;
           } else if (t1 - 1 >= cl - 1) {
             cl = min(cl, t0);
+            qe = q;
           } else {
-            emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0, sl, ns);
+            emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0, sl + qs, qe - qs + 1);
             cl = t0;
             ch = t1 - 1;
+            qs = qe = q;
           }
         }
-        if (ch >= cl) emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0, sl, ns);
+        if (ch >= cl) emit_range(E, kb, cl, ch + 1, R_VSSL, rmode, ii, RW.H, RW.nh, 0, 0, sl + qs, qe - qs + 1);
       }
     }
     return;
@@ -615,8 +621,7 @@ __device__ void emit_main(const IndexCtx& C, const ItemCtx& I, int ii, Emitter& 
 constexpr int LONG_LIVE = 4096;
 __device__ __forceinline__ uint32_t order_key(uint32_t cls, uint32_t v) { return (cls << 30) | (v & 0x3FFFFFFFu); }
 
-__device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W, uint32_t& okey) {
-  // locate the pass
+__device__ __forceinline__ int slot_pass(const IndexCtx& C, int slot) {
   int lo = 0, hi = C.n_passes - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -625,7 +630,11 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W,
     else
       hi = mid - 1;
   }
-  const DPass ps = C.passes[lo];
+  return lo;
+}
+
+__device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W, uint32_t& okey) {
+  const DPass ps = C.passes[slot_pass(C, slot)];
   const int b = slot - ps.slot_base;
   ItemCtx I;
   I.h = ps.head;

@@ -126,6 +126,7 @@ def run_gpu(wl, d, want_fp: bool = True):
     o = torch.full((pb.n_heads, pb.seq_len, pb.head_dim), float("nan"), dtype=torch.bfloat16, device="cuda")
     sp(q, k, v, lab, o=o, lse=lse)
     torch.cuda.synchronize()
+    assert sp.flags() == 0, "device-side flags raised (label range / segment overflow)"
     exps = [parse_export(mmi_export_index(pb, wl.heads, sp.ws, h)) for h in range(pb.n_heads)]
     fp = None
     if want_fp:
