@@ -81,13 +81,21 @@ def count_launches(heads, fused: int = 1) -> int:
         n += 5                              # gather-rank, fold, derive, eval, pick
     if any(p.kind == KIND_VSLASH for p in pats):
         n += 1                              # vs select
-    n += 2 + 1 + 1                          # views (Q, K), inst params, items count
+    n += 1 + 2 + 1 + 1                      # view aliases, views (Q, K), inst params, items count
     n += 2                                  # segment-offset scan (tile sums, tile scan)
     n += 1                                  # items fill
     n += 8                                  # LPT sort: 4 radix passes x (histogram, scatter)
     n += 1                                  # items gather
     n += 0 if fused == 3 else (1 if fused == 1 else 2)  # permute gathers (K/V; Q fused into the attention loads)
     n += 1                                  # sparse attention
+    # kernel byte copies / fills (util.cu; not copy-engine operations): estimate: device tables,
+    # labels; fills of flags, column mass, diagonal mass, VS bitmaps, VS counts, segment counts
+    # (every region has at least one word); sparse: scheduler counter, + NaN fill of partial LSEs
+    # when rows are merged
+    n += 2 + 6
+    merged = any((p.kind == KIND_GRID and (p.use_slash or p.use_hline)) or p.kind in (KIND_SF_STRIDED, KIND_TRISHAPE)
+                 for p in pats)
+    n += 1 + int(merged)
     n += int(any((p.kind == KIND_GRID and p.use_slash) or p.kind == KIND_SF_STRIDED for p in pats))  # LSE merge
     n += int(any((p.kind == KIND_GRID and p.use_hline) or p.kind == KIND_TRISHAPE for p in pats))   # h-row merge
     return n
