@@ -81,9 +81,8 @@ def count_launches(heads, fused: int = 1) -> int:
         n += 5                              # gather-rank, fold, derive, eval, pick
     if any(p.kind == KIND_VSLASH for p in pats):
         n += 1                              # vs select
-    n += 1 + 2 + 1 + 1                      # view aliases, views (Q, K), inst params, items count
-    n += 2                                  # segment-offset scan (tile sums, tile scan)
-    n += 1                                  # items fill
+    n += 1 + 2 + 1                          # view aliases, views (Q, K), inst params
+    n += 1                                  # items fill (static per-slot segment regions: no count, no scan)
     n += 8                                  # LPT sort: 4 radix passes x (histogram, scatter)
     n += 1                                  # items gather
     n += 0 if fused == 3 else (1 if fused == 1 else 2)  # permute gathers (K/V; Q fused into the attention loads)

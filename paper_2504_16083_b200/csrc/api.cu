@@ -205,6 +205,8 @@ static IndexCtx make_ctx(const Plan& P, void* ws) {
   C.sort_vals = at<int>(ws, P.item_vals);
   C.sort_vals_out = at<int>(ws, P.item_vals);
   C.seg_cap = P.seg_cap;
+  C.seg_spill_base = P.seg_spill_base;
+  C.seg_spill_cap = P.seg_spill_cap;
   C.flags = at<unsigned>(ws, P.flags);
   C.part_o = at<__half>(ws, P.part_o);
   C.part_lse = at<float>(ws, P.part_lse);
@@ -292,13 +294,11 @@ extern "C" mmi_status mmi_estimate_index(const mmi_problem* pb, const mmi_head_c
             at<float>(ws, P.cbuf), at<unsigned long long>(ws, P.dgbuf), blob_at<int64_t>(ws, P, P.o_vsl),
             blob_at<int64_t>(ws, P, P.o_vsb), at<int>(ws, P.vs_lists), at<int>(ws, P.vs_cnt),
             at<uint32_t>(ws, P.bits), s);
-  // a5 views, instance parameters, work items (count -> scan -> fill -> LPT sort)
+  // a5 views, instance parameters, work items (fill -> order sort)
   launch_build_views(C, blob_at<int>(ws, P, P.o_qv), (int)P.qview_ids.size(), blob_at<int>(ws, P, P.o_kv),
                      (int)P.kview_ids.size(), P.qg_rows, P.kg_rows, s);
   launch_inst_params(C, (int)P.insts.size(), s);
-  launch_items_count(C, s);
-  launch_scan_exclusive(C.seg_cnt, (int*)C.seg_off, P.n_slots + 1, at<int>(ws, P.scan_tmp), s);
-  launch_items_fill(C, s);
+  launch_items_fill(C, s);  // static per-slot segment regions (+ spill): no count pass, no scan
   // work order: stable ascending sort of the inverted LPT / locality keys (items_fill_kernel)
   launch_sort_pairs(reinterpret_cast<uint32_t*>(C.sort_keys), reinterpret_cast<uint32_t*>(C.sort_keys) + P.n_slots,
                     C.sort_vals, C.sort_vals + P.n_slots, P.n_slots, 32, at<int>(ws, P.sort_tmp), s);

@@ -254,10 +254,11 @@ struct Rows {
 
 struct Emitter {
   Seg* out;        // nullptr => count only
+  int cap;         // segments `out` holds (further ones are counted, not written)
   int n_segs, n_tiles, n_live;  // n_live: live (tile, half) pairs
   __device__ __forceinline__ void add(int krow0, int ntiles, uint32_t meta, const int (&c)[2][5]) {
     if (ntiles <= 0) return;
-    if (out) {
+    if (out && n_segs < cap) {
       Seg s;
       s.krow0 = krow0;
       s.ntiles = ntiles;
@@ -836,32 +837,38 @@ __device__ void build_slot(const IndexCtx& C, int slot, Emitter& E, WorkItem& W,
   }
 }
 
-__global__ void items_count_kernel(IndexCtx C) {
+// One pass over the slots: a slot writes its segments straight into its static region of the pass
+// (seg_base + b * seg_per_slot, the plan's analytic per-slot bound), so no count pass and no scan.
+// A slot whose bound is short (counted while writing) is rebuilt into the spill area; only if
+// that is full too is the item left empty and FLAG_SEG_OVERFLOW raised.
+__global__ void items_fill_kernel(IndexCtx C) {
   const int slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= C.n_slots) return;
+  const DPass ps = C.passes[slot_pass(C, slot)];
+  int off = ps.seg_base + (slot - ps.slot_base) * ps.seg_per_slot;
   Emitter E;
-  E.out = nullptr;
+  E.out = C.segs + off;
+  E.cap = ps.seg_per_slot;
   E.n_segs = E.n_tiles = E.n_live = 0;
   WorkItem W;
   uint32_t okey = 0;
   build_slot(C, slot, E, W, okey);
-  C.seg_cnt[slot] = E.n_segs;
-}
-
-__global__ void items_fill_kernel(IndexCtx C) {
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= C.n_slots) return;
-  Emitter E;
-  const int off = C.seg_off[slot];
-  E.n_segs = E.n_tiles = E.n_live = 0;
-  WorkItem W;
-  if ((int64_t)off + C.seg_cnt[slot] > C.seg_cap) {
-    // the plan's segment bound was short: never write past the region; the item stays empty
-    // (its rows are not computed) and mmi_workspace_flags reports it
+  if (E.n_segs > E.cap) {
+    const int need = E.n_segs;
+    const unsigned long long sp = atomicAdd(reinterpret_cast<unsigned long long*>(C.seg_cnt), (unsigned long long)need);
+    if ((long long)sp + need <= C.seg_spill_cap) {
+      off = (int)(C.seg_spill_base + (long long)sp);
+      E.out = C.segs + off;
+      E.cap = need;
+      E.n_segs = E.n_tiles = E.n_live = 0;
+      okey = 0;
+      build_slot(C, slot, E, W, okey);
+    }
+  }
+  if (E.n_segs > E.cap) {
+    // static region and spill area both short: the item stays empty (its rows are not computed)
+    // and mmi_workspace_flags reports it
     atomicOr(C.flags, FLAG_SEG_OVERFLOW);
-    E.out = nullptr;
-    uint32_t okey = 0;
-    build_slot(C, slot, E, W, okey);
     W.seg_off = off;
     W.n_segs = W.n_tiles = 0;
     W.pad[1] = 0;
@@ -870,9 +877,6 @@ __global__ void items_fill_kernel(IndexCtx C) {
     C.sort_vals[slot] = slot;
     return;
   }
-  E.out = C.segs + off;
-  uint32_t okey = 0;
-  build_slot(C, slot, E, W, okey);
   W.seg_off = off;
   W.n_segs = E.n_segs;
   W.n_tiles = E.n_tiles;
@@ -1103,9 +1107,6 @@ void launch_build_views(const IndexCtx& C, const int* qviews, int nq, const int*
 }
 void launch_inst_params(const IndexCtx& C, int n_total, cudaStream_t st) {
   inst_params_kernel<<<(n_total + 127) / 128, 128, 0, st>>>(C, n_total);
-}
-void launch_items_count(const IndexCtx& C, cudaStream_t st) {
-  items_count_kernel<<<(C.n_slots + 127) / 128, 128, 0, st>>>(C);
 }
 void launch_items_fill(const IndexCtx& C, cudaStream_t st) {
   items_fill_kernel<<<(C.n_slots + 127) / 128, 128, 0, st>>>(C);

@@ -39,13 +39,13 @@ struct IndexCtx {
   const __half* part_o;
   const float* part_lse;
   int64_t seg_cap;      // capacity of segs (plan bound)
+  int64_t seg_spill_base, seg_spill_cap;  // spill area (slots whose static region is too small)
   unsigned* flags;      // device-side error flags (MMI_FLAG_*)
 };
 
 void launch_build_views(const IndexCtx& C, const int* qviews, int nq, const int* kviews, int nk, int64_t qrows,
                         int64_t krows, cudaStream_t st);
 void launch_inst_params(const IndexCtx& C, int n_total, cudaStream_t st);
-void launch_items_count(const IndexCtx& C, cudaStream_t st);
 void launch_items_fill(const IndexCtx& C, cudaStream_t st);
 void launch_items_gather(const IndexCtx& C, cudaStream_t st);
 void launch_gather(const int* src, int64_t rows, int D, const void* a, void* a_out, const void* b, void* b_out,

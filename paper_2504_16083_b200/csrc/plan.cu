@@ -335,6 +335,7 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
     mp.slot_base = slot;
     slot += mp.n_slots;
     P.passes.push_back(mp);
+    const size_t mp_idx = P.passes.size() - 1;
     int64_t per_main = 0;
     for (int a = 0; a < MAX_MOD; ++a) {
       int64_t s = 0;
@@ -344,6 +345,8 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
       }
       per_main = std::max(per_main, s);
     }
+    P.passes[mp_idx].seg_base = (int32_t)segcap;  // (the total is checked against 2^31 below)
+    P.passes[mp_idx].seg_per_slot = (int32_t)(3 * per_main + 2);
     segcap += (3 * per_main + 2) * mp.n_slots;
     for (int i = 0; i < hd.n_inst; ++i) {
       const DInst& x = P.insts[(size_t)h * MAX_INST + i];
@@ -369,6 +372,8 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
         p2.pad0 = n_split;
         p2.n_slots = n_pairs * n_split;
         p2.slot_base = slot;
+        p2.seg_base = (int32_t)segcap;
+        p2.seg_per_slot = (int32_t)(3 + 3 * cross);
         slot += p2.n_slots;
         P.passes.push_back(p2);
         segcap += (3 + 3 * cross) * p2.n_slots;
@@ -391,6 +396,8 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
         p3.qa = (hd.boundary == MMI_BND_Q) ? x.qa : -1;
         p3.n_slots = (P.views[x.v_res_q].cap / BLK + 1) / 2 + x.smax + 1;
         p3.slot_base = slot;
+        p3.seg_base = (int32_t)segcap;
+        p3.seg_per_slot = 3;
         slot += p3.n_slots;
         P.passes.push_back(p3);
         segcap += 3 * p3.n_slots;
@@ -398,7 +405,10 @@ mmi_status build_plan(const mmi_problem* pb, const mmi_head_config* cfg, Plan& P
     }
   }
   P.n_slots = slot;
-  P.seg_cap = segcap + 16;
+  // static per-slot regions, then a spill area for a slot whose analytic bound is short
+  P.seg_spill_base = segcap;
+  P.seg_spill_cap = std::max<int64_t>(segcap / 8, 4096);
+  P.seg_cap = segcap + P.seg_spill_cap + 16;
   P.part_rows = part_rows_hrow_cursor;
 
   // VS lists / bitmaps

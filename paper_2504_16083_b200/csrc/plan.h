@@ -61,6 +61,7 @@ struct DSlab {
 struct DPass {
   int32_t head, pass, inst, n_slots;   // inst: grid instance (HROW/SLASH), -1 for MAIN
   int32_t slot_base, qa, pad0, pad1;   // qa: Q-bnd HROW/SLASH modality filter (-1 none); pad0: HROW key chunks
+  int32_t seg_base, seg_per_slot;      // static segment region of the pass: slot b at seg_base + b * seg_per_slot
 };
 struct DHrow {                         // one h-line (HROW) pass: its split-K partials are merged by hrow_merge
   int32_t head, inst, qa, n_split;
@@ -98,6 +99,7 @@ struct Plan {
   int64_t qg_rows = 0, kg_rows = 0;
   int n_slots = 0;
   int64_t seg_cap = 0;
+  int64_t seg_spill_base = 0, seg_spill_cap = 0;  // spill area after the static per-slot regions
   std::vector<int64_t> slot_seg_cap_prefix;  // not used on device
   int64_t part_rows = 0;
   int n_chunks = 0;                    // slab key chunks
