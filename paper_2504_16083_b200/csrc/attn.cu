@@ -9,17 +9,19 @@
 // executes every pattern / boundary type ("sparse loading with dense
 // computation").
 //
-// Warp roles (one CTA per SM, persistent, static round-robin over LPT-ordered
-// work items):
-//   warp 0     TMA Q loader (one Q tile per work item)
-//   warp 1     MMA issuer: S = Q K^T into TMEM (double buffered), O += P V; TMEM alloc
-//   warp 2     TMA K loader (K ring, + key positions / ranks for PRED tiles)
-//   warp 3     TMA V loader (V ring, decoupled from K so K runs ahead)
-//   warps 4-7  softmax / correction / epilogue, thread t owns query row t
-//              (TMEM lane t): tcgen05.ld S, predicate mask, exp2, P (bf16) -> TMEM
-//              aliasing S (A operand of the P V tcgen05.mma), lazy O rescale in TMEM.
-// Work items are fetched dynamically (atomic counter) by warp 0 and broadcast to
-// the other roles through a 4-deep shared-memory ring.
+// Work item = two 128-row query blocks (halves A and B) sharing one list of key-tile segments
+// with per-half DEAD / PRED / FULL tile states.  One persistent CTA per SM; items are fetched
+// dynamically from the workspace counter (locality / longest-first order) and broadcast to the
+// roles through a 4-deep shared-memory ring.  Warp roles:
+//   warp 0      scheduler + Q loader (permuted Q rows gathered with TMA tile::gather4)
+//   warp 1      MMA issuer (one elected thread): per key tile P_A(t,0)V, P_B(t,0)V, P_A(t,1)V,
+//               S_A(t+1), P_B(t,1)V, S_B(t+1) (S = one M128 N128 group per half); TMEM alloc
+//   warp 2      K TMA ring (+ key positions / ranks of gathered tiles that are masked)
+//   warp 3      V TMA ring (decoupled from K so K runs ahead)
+//   warps 4-11  softmax / correction / epilogue, one warpgroup per half; thread t owns query row
+//               t (TMEM lane t): tcgen05.ld S, predicate mask, exp2, P (bf16) -> TMEM aliasing S
+//               (A operand of the P V tcgen05.mma), lazy O rescale, O -> bf16 / fp16 stores.
+// Measured alternatives and the per-event timeline: DESIGN.md 6.1-6.2, profiles/r2_ab_attention.md.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
