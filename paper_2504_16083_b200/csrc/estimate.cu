@@ -571,7 +571,10 @@ __device__ __forceinline__ void grid_window(const DInst& x, const int* sinfo, co
 #define MMI_FOLD_CHUNK 8192
 #endif
 constexpr int FOLD_CHUNK = MMI_FOLD_CHUNK;   // u32 keys per shared-memory chunk (32 KB)
-constexpr int FOLD_SPC = 8;                  // candidate strides per CTA
+#ifndef MMI_FOLD_SPC
+#define MMI_FOLD_SPC 2
+#endif
+constexpr int FOLD_SPC = MMI_FOLD_SPC;       // candidate strides per CTA
 constexpr int FOLD_THREADS = 256;
 constexpr int FOLD_MAXW = 4;                 // phases per thread for strides in (256, 1024]
 
