@@ -24,7 +24,10 @@ namespace mmi {
 
 constexpr int STC_THREADS = 256;   // warp 0 TMA, warp 1 MMA + TMEM, warps 2-3 Q staging, warps 4-7 epilogue
 constexpr int STC_KST = 2;         // K ring stages
-constexpr int STC_CHUNK_TILES = 64;  // key tiles per CTA (8192 keys)
+#ifndef MMI_STC_CHUNK
+#define MMI_STC_CHUNK 32
+#endif
+constexpr int STC_CHUNK_TILES = MMI_STC_CHUNK;  // key tiles per CTA (4096 keys; 8192 measured 4 % slower at 128K)
 
 template <int D>
 struct StcSmem {
